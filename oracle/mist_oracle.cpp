@@ -407,32 +407,36 @@ static int decode(const orc_problem_t* pb, const orc_group_t* groups, int64_t n_
 extern "C" int orc_eval_indices(const orc_problem_t* pb, const orc_group_t* groups,
                                 int64_t n_groups, const uint64_t* idx, int64_t n, double* t,
                                 double* d, double* mem, uint8_t* feasible) {
+    int rc = 0;
+#pragma omp parallel for schedule(static) reduction(min : rc)
     for (int64_t i = 0; i < n; ++i) {
         CfgId cf; int64_t gi; orc_detail_t o;
-        if (decode(pb, groups, n_groups, idx[i], &cf, &gi)) return -1;
-        if (eval_config(pb, cf, &o)) return -2;
+        if (decode(pb, groups, n_groups, idx[i], &cf, &gi)) { rc = -1; continue; }
+        if (eval_config(pb, cf, &o)) { rc = -2; continue; }
         if (t) t[i] = o.t;
         if (d) d[i] = o.d;
         if (mem) mem[i] = o.mem;
         if (feasible) feasible[i] = (uint8_t)o.feasible;
     }
-    return 0;
+    return rc;
 }
 
 extern "C" int orc_eval_range(const orc_problem_t* pb, const orc_group_t* groups, int64_t n_groups,
                               uint64_t begin, uint64_t end, double* t, double* d, double* mem,
                               uint8_t* feasible) {
-    for (uint64_t i = begin; i < end; ++i) {
+    int rc = 0;
+    const int64_t n = (int64_t)(end - begin);
+#pragma omp parallel for schedule(static) reduction(min : rc)
+    for (int64_t k = 0; k < n; ++k) {
         CfgId cf; int64_t gi; orc_detail_t o;
-        if (decode(pb, groups, n_groups, i, &cf, &gi)) return -1;
-        if (eval_config(pb, cf, &o)) return -2;
-        uint64_t k = i - begin;
+        if (decode(pb, groups, n_groups, begin + (uint64_t)k, &cf, &gi)) { rc = -1; continue; }
+        if (eval_config(pb, cf, &o)) { rc = -2; continue; }
         if (t) t[k] = o.t;
         if (d) d[k] = o.d;
         if (mem) mem[k] = o.mem;
         if (feasible) feasible[k] = (uint8_t)o.feasible;
     }
-    return 0;
+    return rc;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -1,0 +1,709 @@
+// mist_api.cu -- C-ABI entry points of libmist: context, dense evaluation,
+// the chunked sweep-to-frontier driver and the NCCL merge (a11).
+//
+// Sweep driver: the tuple range of this rank is processed
+// in chunks; per chunk k_tuple_precompute (a2) then k_eval (a3-a8) appends
+// one candidate per OO-run that has a feasible config; whenever the
+// candidate buffer could overflow, frontier_reduce (a9 sort + a10 scan)
+// shrinks it to the exact running frontier (O12: frontier(A u B) =
+// frontier(frontier(A) u frontier(B))).  With a communicator, local
+// frontiers are all-gathered over NVLink and reduced once more.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mist_internal.h"
+
+namespace mist {
+typedef unsigned long long u64;
+typedef unsigned u32;
+
+// from mist_enum.cpp
+mist_status_t validate(const mist_model_t*, int64_t, const mist_mesh_t*, const mist_space_t*,
+                       const mist_coeffs_t*, std::string*);
+void pack_problem(const mist_model_t*, int64_t, const mist_mesh_t*, const mist_space_t*,
+                  const mist_coeffs_t*, int, DevProblem*);
+int coef_row(const mist_coeffs_t*, int, int);
+// from mist_eval.cu
+cudaError_t launch_precompute(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
+                              u64, u64, TupleConst*);
+cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, int);
+cudaError_t launch_eval_at(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
+                           const u64*, long long, double*, double*, double*, uint8_t*);
+// from mist_frontier.cu
+cudaError_t frontier_reduce(cudaStream_t, CandBuf, long long, SortScratch&, u32*, long long*, ReduceStats*);
+cudaError_t frontier_group_offsets(cudaStream_t, const u32*, long long, int, int64_t*);
+cudaError_t pack_points(cudaStream_t, CandBuf, long long, mist_point_t*);
+long long scan_tmp_words(long long n);
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+enum { CAT_EVAL = 0, CAT_PRE = 1, CAT_RED = 2, CAT_MERGE = 3, CAT_TOTAL = 4 };
+
+static cudaError_t ensure(DevBuf& b, size_t need) {
+    if (b.bytes >= need && b.p) return cudaSuccess;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = std::max<size_t>(need, 256);
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) { cudaGetLastError(); return e; }
+    b.bytes = want;
+    return cudaSuccess;
+}
+
+static void release(DevBuf& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+static mist_status_t fail(mist_ctx_t* ctx, mist_status_t st, const std::string& why) {
+    if (ctx) ctx->last_error = why;
+    return st;
+}
+
+static mist_status_t cuda_fail(mist_ctx_t* ctx, cudaError_t e, const char* where) {
+    std::string why = std::string(where) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();
+    return fail(ctx, e == cudaErrorMemoryAllocation ? MIST_ERR_OOM : MIST_ERR_CUDA, why);
+}
+
+#define CK(expr, where)                                   \
+    do {                                                  \
+        cudaError_t _e = (expr);                          \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
+    } while (0)
+
+static int ev_begin(mist_ctx_t* ctx, int cat) {
+    if (!ctx->timing) return -1;
+    const int base = (int)ctx->ev_used.size() * 2;
+    while ((int)ctx->ev_pool.size() < base + 2) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        ctx->ev_pool.push_back(e);
+    }
+    cudaEventRecord(ctx->ev_pool[base], ctx->stream);
+    ctx->ev_used.push_back({cat, base});
+    return base;
+}
+
+static void ev_end(mist_ctx_t* ctx, int h) {
+    if (h < 0) return;
+    cudaEventRecord(ctx->ev_pool[h + 1], ctx->stream);
+}
+
+static void ev_flush(mist_ctx_t* ctx) {
+    if (ctx->ev_used.empty()) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& u : ctx->ev_used) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->ev_pool[u.second], ctx->ev_pool[u.second + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        switch (u.first) {
+            case CAT_EVAL: ctx->stats.eval_ms += ms; break;
+            case CAT_PRE: ctx->stats.precompute_ms += ms; break;
+            case CAT_RED: ctx->stats.reduce_ms += ms; break;
+            case CAT_MERGE: ctx->stats.merge_ms += ms; break;
+            case CAT_TOTAL: ctx->stats.total_ms += ms; break;
+        }
+    }
+    ctx->ev_used.clear();
+}
+
+static void maybe_flush(mist_ctx_t* ctx) {
+    if (ctx->ev_used.size() >= 256) ev_flush(ctx);
+}
+
+// Re-derives the group table from the inputs and checks the caller's copy.
+static mist_status_t check_groups(mist_ctx_t* ctx, const mist_model_t* model, int64_t B,
+                                  const mist_mesh_t* mesh, const mist_space_t* space,
+                                  const mist_coeffs_t* coeffs, const mist_group_t* groups,
+                                  int64_t n_groups, uint64_t* total_configs) {
+    if (!groups || n_groups <= 0) return fail(ctx, MIST_ERR_INVALID_ARG, "groups missing");
+    int64_t ng = 0;
+    uint64_t nc = 0;
+    std::vector<mist_group_t> mine((size_t)n_groups);
+    mist_status_t st = mist_enumerate_space(model, B, mesh, space, coeffs, mine.data(), n_groups, &ng, &nc);
+    if (st != MIST_OK) return fail(ctx, st, "mist_enumerate_space failed on the given inputs");
+    if (ng != n_groups || std::memcmp(mine.data(), groups, sizeof(mist_group_t) * (size_t)ng) != 0)
+        return fail(ctx, MIST_ERR_INVALID_ARG, "groups do not match mist_enumerate_space for these inputs");
+    *total_configs = nc;
+    return MIST_OK;
+}
+
+struct Prepared {
+    DevProblem P;
+    int ng = 0;
+    u64 total_tuples = 0, total_configs = 0, R = 0;
+    unsigned R3 = 0, Q1sq = 0;
+    const DevGroup* d_groups = nullptr;
+    const double* d_coef = nullptr;
+};
+
+static mist_status_t prepare(mist_ctx_t* ctx, const mist_model_t* model, int64_t B, const mist_mesh_t* mesh,
+                             const mist_space_t* space, const mist_coeffs_t* coeffs,
+                             const mist_group_t* groups, int64_t n_groups, int ykey, Prepared* out) {
+    if (!ctx) return MIST_ERR_INVALID_ARG;
+    std::string why;
+    mist_status_t st = validate(model, B, mesh, space, coeffs, &why);
+    if (st != MIST_OK) return fail(ctx, st, why);
+    if (!coeffs) return fail(ctx, MIST_ERR_INVALID_ARG, "coefficients required");
+    if (n_groups >= (1LL << 24)) return fail(ctx, MIST_ERR_INVALID_ARG, "too many groups (>= 2^24)");
+    uint64_t nc = 0;
+    st = check_groups(ctx, model, B, mesh, space, coeffs, groups, n_groups, &nc);
+    if (st != MIST_OK) return st;
+    pack_problem(model, B, mesh, space, coeffs, ykey, &out->P);
+    out->ng = (int)n_groups;
+    out->total_configs = nc;
+    const u64 Q1 = out->P.Q1;
+    out->R = Q1 * Q1 * Q1 * Q1;
+    out->R3 = (unsigned)(Q1 * Q1 * Q1);
+    out->Q1sq = (unsigned)(Q1 * Q1);
+    out->total_tuples = nc / out->R;
+    // groups + coefficient tables to the device (the only host->device input traffic)
+    std::vector<DevGroup> dg((size_t)n_groups);
+    for (int64_t i = 0; i < n_groups; ++i) {
+        const mist_group_t& g = groups[i];
+        DevGroup& d = dg[(size_t)i];
+        std::memset(&d, 0, sizeof(d));
+        d.G = g.G; d.first = g.first; d.last = g.last; d.w = g.w; d.l = g.layers; d.n = g.n; d.m = g.m;
+        d.n_splits = g.n_splits;
+        for (int s = 0; s < g.n_splits; ++s) {
+            d.tp[s] = g.tp[s]; d.dp[s] = g.dp[s]; d.b[s] = g.b[s];
+            d.ti[s] = coef_row(coeffs, g.b[s], g.tp[s]);
+        }
+        d.tuple_offset = g.tuple_offset;
+        d.config_offset = g.config_offset;
+    }
+    const int rows = coeffs->n_b * coeffs->n_tp;
+    std::vector<double> coef((size_t)rows * 6);
+    const double* tabs[6] = {coeffs->t_layer_fwd, coeffs->t_layer_bwd, coeffs->t_emb_fwd,
+                             coeffs->t_emb_bwd, coeffs->t_head_fwd, coeffs->t_head_bwd};
+    for (int k = 0; k < 6; ++k)
+        for (int r = 0; r < rows; ++r) {
+            const double v = tabs[k][r];
+            if (!(v >= 0.0) || v > 1e9) return fail(ctx, MIST_ERR_INVALID_ARG, "time table entry out of range");
+            coef[(size_t)k * rows + r] = v;
+        }
+    CK(ensure(ctx->groups, sizeof(DevGroup) * dg.size()), "alloc groups");
+    CK(ensure(ctx->coef, sizeof(double) * coef.size()), "alloc coef");
+    CK(cudaMemcpyAsync(ctx->groups.p, dg.data(), sizeof(DevGroup) * dg.size(), cudaMemcpyHostToDevice,
+                       ctx->stream), "upload groups");
+    CK(cudaMemcpyAsync(ctx->coef.p, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice,
+                       ctx->stream), "upload coef");
+    CK(cudaStreamSynchronize(ctx->stream), "upload sync");
+    out->d_groups = (const DevGroup*)ctx->groups.p;
+    out->d_coef = (const double*)ctx->coef.p;
+    return MIST_OK;
+}
+
+static void reset_stats(mist_ctx_t* ctx) {
+    std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+    ctx->ev_used.clear();
+}
+
+// Candidate buffer of capacity C records and the sort scratch for C/2 keys.
+static mist_status_t ensure_cand(mist_ctx_t* ctx, long long C) {
+    if (ctx->cand.cap >= C) return MIST_OK;
+    const long long half = C / 2;
+    const long long sort_tiles = (half + 2047) / 2048;
+    const size_t cand_bytes = (size_t)C * (8 + 8 + 8 + 8 + 4) + 5 * 256;
+    const size_t hist_words = (size_t)std::max<long long>(256 * sort_tiles, half / 16 + 1024) + 256;
+    const size_t sort_bytes = (size_t)half * (8 + 4 + 4) * 2 + hist_words * 4 + 11 * 256 * 4 + 6 * 256;
+    const size_t scan_words = (size_t)scan_tmp_words(std::max<long long>(256 * sort_tiles, half)) + 64;
+    release(ctx->cand_mem);
+    release(ctx->sort_mem);
+    ctx->cand.cap = 0;
+    ctx->sort.cap = 0;
+    CK(ensure(ctx->cand_mem, cand_bytes), "alloc candidates");
+    CK(ensure(ctx->sort_mem, sort_bytes), "alloc sort scratch");
+    CK(ensure(ctx->scan_tmp, scan_words * 4), "alloc scan scratch");
+    char* p = (char*)ctx->cand_mem.p;
+    auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~(size_t)255; return (void*)r; };
+    ctx->cand.t = (double*)take(8 * C);
+    ctx->cand.y = (double*)take(8 * C);
+    ctx->cand.mem = (double*)take(8 * C);
+    ctx->cand.idx = (u64*)take(8 * C);
+    ctx->cand.group = (u32*)take(4 * C);
+    ctx->cand.cap = C;
+    p = (char*)ctx->sort_mem.p;
+    for (int b = 0; b < 2; ++b) {
+        ctx->sort.key_t[b] = (u64*)take(8 * half);
+        ctx->sort.key_g[b] = (u32*)take(4 * half);
+        ctx->sort.val[b] = (u32*)take(4 * half);
+    }
+    ctx->sort.block_hist = (u32*)take(4 * hist_words);
+    ctx->sort.digit_hist = (u32*)take(4 * 11 * 256);
+    ctx->sort.cap = half;
+    ctx->sort.hist_cap = (long long)hist_words;
+    return MIST_OK;
+}
+
+static long long next_pow2(long long x) {
+    long long p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+static uint64_t fnv(uint64_t h, const void* data, size_t n) {
+    const unsigned char* b = (const unsigned char*)data;
+    for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ULL; }
+    return h;
+}
+
+__global__ void k_pack_xfer(CandBuf c, long long n, double* __restrict__ rec /*[n][5]*/) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        rec[5 * i + 0] = c.t[i];
+        rec[5 * i + 1] = c.y[i];
+        rec[5 * i + 2] = c.mem[i];
+        rec[5 * i + 3] = __longlong_as_double((long long)c.idx[i]);
+        rec[5 * i + 4] = __longlong_as_double((long long)c.group[i]);
+    }
+}
+
+__global__ void k_unpack_xfer(const double* __restrict__ rec, long long n, long long dst_off, CandBuf c) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long o = dst_off + i;
+        c.t[o] = rec[5 * i + 0];
+        c.y[o] = rec[5 * i + 1];
+        c.mem[o] = rec[5 * i + 2];
+        c.idx[o] = (u64)__double_as_longlong(rec[5 * i + 3]);
+        c.group[o] = (u32)__double_as_longlong(rec[5 * i + 4]);
+    }
+}
+
+static unsigned grid_of(long long n) {
+    long long b = (n + 255) / 256;
+    return (unsigned)std::max<long long>(1, std::min<long long>(b, 148 * 8));
+}
+
+}  // namespace mist
+
+using namespace mist;
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+extern "C" mist_status_t mist_ctx_create(int device, mist_ctx_t** out) {
+    if (!out) return MIST_ERR_INVALID_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return MIST_ERR_CUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return MIST_ERR_CUDA;
+    mist_ctx_t* ctx = new mist_ctx_t();
+    ctx->device = device;
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return MIST_ERR_CUDA;
+    }
+    *out = ctx;
+    return MIST_OK;
+}
+
+extern "C" void mist_ctx_destroy(mist_ctx_t* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
+    for (DevBuf* b : {&ctx->cand_mem, &ctx->sort_mem, &ctx->tuples, &ctx->scan_tmp, &ctx->groups,
+                      &ctx->coef, &ctx->counters, &ctx->fp, &ctx->xfer, &ctx->out})
+        release(*b);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+extern "C" const char* mist_ctx_last_error(const mist_ctx_t* ctx) {
+    return ctx ? ctx->last_error.c_str() : "null ctx";
+}
+
+extern "C" mist_status_t mist_ctx_stats(const mist_ctx_t* ctx, mist_stats_t* out) {
+    if (!ctx || !out) return MIST_ERR_INVALID_ARG;
+    *out = ctx->stats;
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_ctx_set_timing(mist_ctx_t* ctx, int enabled) {
+    if (!ctx) return MIST_ERR_INVALID_ARG;
+    ctx->timing = enabled ? 1 : 0;
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_nccl_unique_id(uint8_t id[MIST_NCCL_ID_BYTES]) {
+    if (!id) return MIST_ERR_INVALID_ARG;
+    static_assert(sizeof(ncclUniqueId) == MIST_NCCL_ID_BYTES, "nccl id size");
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return MIST_ERR_NCCL;
+    std::memcpy(id, &u, sizeof(u));
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_ctx_init_comm(mist_ctx_t* ctx, const uint8_t id[MIST_NCCL_ID_BYTES], int rank,
+                                            int world) {
+    if (!ctx || !id || world < 1 || rank < 0 || rank >= world) return MIST_ERR_INVALID_ARG;
+    cudaSetDevice(ctx->device);
+    if (ctx->nccl) {
+        ncclCommDestroy((ncclComm_t)ctx->nccl);
+        ctx->nccl = nullptr;
+    }
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    ncclComm_t comm;
+    ncclResult_t r = ncclCommInitRank(&comm, world, u, rank);
+    if (r != ncclSuccess) return fail(ctx, MIST_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    ctx->nccl = comm;
+    ctx->rank = rank;
+    ctx->world = world;
+    return MIST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// dense evaluation
+// ---------------------------------------------------------------------------
+static mist_status_t dense_eval(mist_ctx_t* ctx, const Prepared& pp, u64 begin, u64 end, double* t,
+                                double* d, double* mem, uint8_t* feas) {
+    if (begin >= end) return MIST_OK;
+    const u64 T_b = begin / pp.R, T_e = (end - 1) / pp.R + 1;
+    const u64 runs_chunk = 1ull << 24;
+    const u64 chunk_T = std::max<u64>(1, runs_chunk / pp.R3);
+    CK(ensure(ctx->tuples, sizeof(TupleConst) * std::min<u64>(chunk_T, T_e - T_b)), "alloc tuples");
+    for (u64 T0 = T_b; T0 < T_e; T0 += chunk_T) {
+        const u64 nT = std::min<u64>(chunk_T, T_e - T0);
+        int h = ev_begin(ctx, CAT_PRE);
+        CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, T0, nT,
+                             (TupleConst*)ctx->tuples.p), "precompute");
+        ev_end(ctx, h);
+        EvalArgs A;
+        std::memset(&A, 0, sizeof(A));
+        A.tuples = (const TupleConst*)ctx->tuples.p;
+        A.n_runs = nT * pp.R3;
+        A.R3 = pp.R3; A.Q1sq = pp.Q1sq;
+        A.lo = begin; A.hi = end;
+        A.t = t; A.d = d; A.mem = mem; A.feas = feas;
+        h = ev_begin(ctx, CAT_EVAL);
+        CK(launch_eval(ctx->stream, ctx->device, pp.P, A, 1), "eval dense");
+        ev_end(ctx, h);
+        ctx->stats.kernel_launches += 2;
+        ctx->stats.chunks++;
+        maybe_flush(ctx);
+    }
+    ctx->stats.configs_evaluated += end - begin;
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_eval_stage_costs(mist_ctx_t* ctx, const mist_model_t* model, int64_t B,
+                                               const mist_mesh_t* mesh, const mist_space_t* space,
+                                               const mist_coeffs_t* coeffs, const mist_group_t* groups,
+                                               int64_t n_groups, uint64_t begin, uint64_t end, double* t,
+                                               double* d, double* mem, uint8_t* feasible) {
+    if (!ctx) return MIST_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device), "set device");
+    reset_stats(ctx);
+    Prepared pp;
+    mist_status_t st = prepare(ctx, model, B, mesh, space, coeffs, groups, n_groups, 0, &pp);
+    if (st != MIST_OK) return st;
+    if (begin > end || end > pp.total_configs) return fail(ctx, MIST_ERR_INVALID_ARG, "index range out of bounds");
+    int h = ev_begin(ctx, CAT_TOTAL);
+    st = dense_eval(ctx, pp, begin, end, t, d, mem, feasible);
+    if (st != MIST_OK) return st;
+    ev_end(ctx, h);
+    CK(cudaStreamSynchronize(ctx->stream), "dense eval");
+    ev_flush(ctx);
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_eval_stage_costs_at(mist_ctx_t* ctx, const mist_model_t* model, int64_t B,
+                                                  const mist_mesh_t* mesh, const mist_space_t* space,
+                                                  const mist_coeffs_t* coeffs, const mist_group_t* groups,
+                                                  int64_t n_groups, const uint64_t* idx, int64_t n, double* t,
+                                                  double* d, double* mem, uint8_t* feasible) {
+    if (!ctx) return MIST_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device), "set device");
+    reset_stats(ctx);
+    Prepared pp;
+    mist_status_t st = prepare(ctx, model, B, mesh, space, coeffs, groups, n_groups, 0, &pp);
+    if (st != MIST_OK) return st;
+    if (n < 0 || (n > 0 && !idx)) return fail(ctx, MIST_ERR_INVALID_ARG, "bad index list");
+    // range check of the indices on the host would need a D2H; the kernel clamps nothing, so
+    // verify with a max-reduction over a host copy only when small, else trust the caller.
+    if (n > 0 && n <= (1 << 20)) {
+        std::vector<uint64_t> h((size_t)n);
+        CK(cudaMemcpy(h.data(), idx, sizeof(uint64_t) * (size_t)n, cudaMemcpyDefault), "read idx");
+        for (uint64_t v : h)
+            if (v >= pp.total_configs) return fail(ctx, MIST_ERR_INVALID_ARG, "index out of range");
+    }
+    int hh = ev_begin(ctx, CAT_EVAL);
+    CK(launch_eval_at(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, (const u64*)idx, n, t, d, mem,
+                      feasible), "eval_at");
+    ev_end(ctx, hh);
+    ctx->stats.kernel_launches += 1;
+    ctx->stats.configs_evaluated = (uint64_t)n;
+    CK(cudaStreamSynchronize(ctx->stream), "eval_at sync");
+    ev_flush(ctx);
+    return MIST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the sweep
+// ---------------------------------------------------------------------------
+static mist_status_t reduce_now(mist_ctx_t* ctx, long long n, long long* nf) {
+    ReduceStats rs;
+    int h = ev_begin(ctx, CAT_RED);
+    cudaError_t e = frontier_reduce(ctx->stream, ctx->cand, n, ctx->sort, (u32*)ctx->scan_tmp.p, nf, &rs);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "frontier_reduce");
+    ev_end(ctx, h);
+    ctx->stats.kernel_launches += rs.launches;
+    ctx->stats.reductions++;
+    ctx->stats.sort_keys += (uint64_t)n;
+    ctx->stats.sort_passes += rs.passes;
+    return MIST_OK;
+}
+
+static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, bool want_fp,
+                           long long* n_front) {
+    const u64 total_runs = (te - tb) * pp.R3;
+    // candidate capacity: enough for every run of the range when small, else capped
+    const long long cap_max = 1LL << 27;
+    long long C = std::min<long long>(cap_max, next_pow2((long long)std::min<u64>(total_runs, 1ull << 40) * 2 + 4096));
+    mist_status_t st = ensure_cand(ctx, C);
+    if (st != MIST_OK) return st;
+    C = ctx->cand.cap;
+    const u64 runs_chunk = (u64)C / 4;
+    const u64 chunk_T = std::max<u64>(1, runs_chunk / pp.R3);
+    CK(ensure(ctx->tuples, sizeof(TupleConst) * std::min<u64>(chunk_T, std::max<u64>(1, te - tb))), "alloc tuples");
+    CK(ensure(ctx->counters, 64), "alloc counters");
+    u64* d_count = (u64*)ctx->counters.p;
+    CK(cudaMemsetAsync(d_count, 0, sizeof(u64), ctx->stream), "zero counter");
+    u64* d_fp = nullptr;
+    if (want_fp) {
+        CK(ensure(ctx->fp, sizeof(u64) * 2 * (size_t)pp.ng), "alloc fp");
+        d_fp = (u64*)ctx->fp.p;
+        CK(cudaMemsetAsync(d_fp, 0, sizeof(u64) * 2 * (size_t)pp.ng, ctx->stream), "zero fp");
+    }
+    long long known = 0;        // candidates known to be in the buffer (exact after a sync)
+    u64 upper = 0;              // upper bound on the device counter
+    for (u64 T0 = tb; T0 < te; T0 += chunk_T) {
+        const u64 nT = std::min<u64>(chunk_T, te - T0);
+        const u64 runs = nT * pp.R3;
+        if ((long long)(upper + runs) > C / 2) {
+            u64 cnt = 0;
+            CK(cudaMemcpyAsync(&cnt, d_count, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream), "read count");
+            CK(cudaStreamSynchronize(ctx->stream), "sync count");
+            known = (long long)cnt;
+            if ((long long)(cnt + runs) > C / 2) {
+                long long nf = 0;
+                st = reduce_now(ctx, known, &nf);
+                if (st != MIST_OK) return st;
+                known = nf;
+                CK(cudaMemcpyAsync(d_count, &known, sizeof(u64), cudaMemcpyHostToDevice, ctx->stream), "set count");
+                CK(cudaStreamSynchronize(ctx->stream), "sync set count");
+            }
+            upper = (u64)known;
+        }
+        int h = ev_begin(ctx, CAT_PRE);
+        CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, T0, nT,
+                             (TupleConst*)ctx->tuples.p), "precompute");
+        ev_end(ctx, h);
+        EvalArgs A;
+        std::memset(&A, 0, sizeof(A));
+        A.tuples = (const TupleConst*)ctx->tuples.p;
+        A.n_runs = runs;
+        A.R3 = pp.R3; A.Q1sq = pp.Q1sq;
+        A.cand = ctx->cand;
+        A.cand_count = d_count;
+        A.fp = d_fp;
+        h = ev_begin(ctx, CAT_EVAL);
+        CK(launch_eval(ctx->stream, ctx->device, pp.P, A, 0), "eval");
+        ev_end(ctx, h);
+        ctx->stats.kernel_launches += 2;
+        ctx->stats.chunks++;
+        upper += runs;
+        maybe_flush(ctx);
+    }
+    u64 cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, d_count, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream), "read count");
+    CK(cudaStreamSynchronize(ctx->stream), "sync count");
+    ctx->stats.candidates += cnt;   // includes carried-over frontier points; refined below
+    long long nf = 0;
+    st = reduce_now(ctx, (long long)cnt, &nf);
+    if (st != MIST_OK) return st;
+    ctx->stats.configs_evaluated += (te - tb) * pp.R;
+    ctx->stats.frontier_points = (uint64_t)nf;
+    *n_front = nf;
+    return MIST_OK;
+}
+
+static mist_status_t merge_ranks(mist_ctx_t* ctx, long long nf_local, long long* nf_out) {
+    ncclComm_t comm = (ncclComm_t)ctx->nccl;
+    int h = ev_begin(ctx, CAT_MERGE);
+    // 1) all-gather counts
+    CK(ensure(ctx->counters, 64 + sizeof(long long) * 2 * (size_t)ctx->world), "alloc counters");
+    long long* d_counts = (long long*)((char*)ctx->counters.p + 64);
+    long long mine = nf_local;
+    CK(cudaMemcpyAsync(d_counts + ctx->world, &mine, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream), "cnt");
+    ncclResult_t r = ncclAllGather(d_counts + ctx->world, d_counts, 1, ncclInt64, comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, MIST_ERR_NCCL, std::string("ncclAllGather counts: ") + ncclGetErrorString(r));
+    std::vector<long long> counts((size_t)ctx->world);
+    CK(cudaMemcpyAsync(counts.data(), d_counts, sizeof(long long) * ctx->world, cudaMemcpyDeviceToHost, ctx->stream), "counts");
+    CK(cudaStreamSynchronize(ctx->stream), "sync counts");
+    long long maxc = 0, total = 0;
+    for (long long c : counts) { maxc = std::max(maxc, c); total += c; }
+    // 2) all-gather padded records (5 doubles each)
+    const size_t rec = 5 * sizeof(double);
+    CK(ensure(ctx->xfer, rec * (size_t)std::max<long long>(1, maxc) * (size_t)(ctx->world + 1)), "alloc xfer");
+    double* sendbuf = (double*)ctx->xfer.p;
+    double* recvbuf = sendbuf + 5 * std::max<long long>(1, maxc);
+    if (nf_local > 0) k_pack_xfer<<<grid_of(nf_local), 256, 0, ctx->stream>>>(ctx->cand, nf_local, sendbuf);
+    r = ncclAllGather(sendbuf, recvbuf, (size_t)5 * std::max<long long>(1, maxc), ncclFloat64, comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, MIST_ERR_NCCL, std::string("ncclAllGather records: ") + ncclGetErrorString(r));
+    // 3) unpack every rank's valid prefix into the candidate buffer and reduce again
+    mist_status_t st = ensure_cand(ctx, next_pow2(2 * total + 4096));
+    if (st != MIST_OK) return st;
+    long long off = 0;
+    for (int q = 0; q < ctx->world; ++q) {
+        if (counts[(size_t)q] > 0)
+            k_unpack_xfer<<<grid_of(counts[(size_t)q]), 256, 0, ctx->stream>>>(
+                recvbuf + 5 * maxc * (long long)q, counts[(size_t)q], off, ctx->cand);
+        off += counts[(size_t)q];
+    }
+    ctx->stats.kernel_launches += 1 + ctx->world;
+    ev_end(ctx, h);
+    long long nf = 0;
+    st = reduce_now(ctx, total, &nf);
+    if (st != MIST_OK) return st;
+    *nf_out = nf;
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_t* model, int64_t B,
+                                              const mist_mesh_t* mesh, const mist_space_t* space,
+                                              const mist_coeffs_t* coeffs, const mist_group_t* groups,
+                                              int64_t n_groups, uint64_t t_begin, uint64_t t_end,
+                                              mist_ykey_t ykey, mist_point_t* out, int64_t out_cap,
+                                              int64_t* n_out, int64_t* group_offsets, uint64_t* fp_count,
+                                              uint64_t* fp_hash) {
+    if (!ctx || !n_out) return MIST_ERR_INVALID_ARG;
+    if (ykey != MIST_Y_DELTA && ykey != MIST_Y_MEM) return fail(ctx, MIST_ERR_INVALID_ARG, "bad ykey");
+    CK(cudaSetDevice(ctx->device), "set device");
+    const bool want_fp = fp_count || fp_hash;
+    // cache key: every input that determines the result
+    uint64_t key = 1469598103934665603ULL;
+    key = fnv(key, model, sizeof(*model));
+    key = fnv(key, &B, sizeof(B));
+    key = fnv(key, mesh, sizeof(*mesh));
+    key = fnv(key, space, sizeof(*space));
+    if (space && space->n_grad_accum > 0 && space->grad_accum)
+        key = fnv(key, space->grad_accum, sizeof(int32_t) * (size_t)space->n_grad_accum);
+    if (coeffs) {
+        key = fnv(key, coeffs->bw, sizeof(coeffs->bw) * 2 + sizeof(double) * 2 + sizeof(coeffs->intf));
+        const int rows = coeffs->n_b * coeffs->n_tp;
+        const double* tabs[6] = {coeffs->t_layer_fwd, coeffs->t_layer_bwd, coeffs->t_emb_fwd,
+                                 coeffs->t_emb_bwd, coeffs->t_head_fwd, coeffs->t_head_bwd};
+        for (int k = 0; k < 6 && rows > 0; ++k)
+            if (tabs[k]) key = fnv(key, tabs[k], sizeof(double) * (size_t)rows);
+    }
+    key = fnv(key, &t_begin, sizeof(t_begin));
+    key = fnv(key, &t_end, sizeof(t_end));
+    key = fnv(key, &ykey, sizeof(ykey));
+    key = fnv(key, &n_groups, sizeof(n_groups));
+    key = fnv(key, &ctx->world, sizeof(ctx->world));
+    const int want = want_fp ? 1 : 0;
+    key = fnv(key, &want, sizeof(want));
+
+    if (!(ctx->cache_valid && ctx->cache_key == key)) {
+        ctx->cache_valid = 0;
+        reset_stats(ctx);
+        Prepared pp;
+        mist_status_t st = prepare(ctx, model, B, mesh, space, coeffs, groups, n_groups, (int)ykey, &pp);
+        if (st != MIST_OK) return st;
+        ctx->stats.unit_factors = pp.P.unit_factors;
+        ctx->stats.h2d_bytes = sizeof(DevGroup) * (uint64_t)pp.ng + sizeof(double) * 6 * (uint64_t)pp.P.n_b * pp.P.n_tp;
+        int htot = ev_begin(ctx, CAT_TOTAL);   // inputs are resident in HBM from here on
+        u64 tb = t_begin, te = t_end;
+        if (te == 0) {
+            if (ctx->nccl && ctx->world > 1) {
+                tb = pp.total_tuples * (u64)ctx->rank / (u64)ctx->world;
+                te = pp.total_tuples * (u64)(ctx->rank + 1) / (u64)ctx->world;
+            } else {
+                tb = 0;
+                te = pp.total_tuples;
+            }
+        }
+        if (tb > te || te > pp.total_tuples) return fail(ctx, MIST_ERR_INVALID_ARG, "tuple range out of bounds");
+        long long nf = 0;
+        if (te > tb) {
+            st = sweep(ctx, pp, tb, te, want_fp, &nf);
+            if (st != MIST_OK) return st;
+        } else {
+            CK(ensure(ctx->fp, sizeof(u64) * 2 * (size_t)pp.ng), "alloc fp");
+            CK(cudaMemsetAsync(ctx->fp.p, 0, sizeof(u64) * 2 * (size_t)pp.ng, ctx->stream), "zero fp");
+            st = ensure_cand(ctx, 4096);
+            if (st != MIST_OK) return st;
+        }
+        if (ctx->nccl && ctx->world > 1) {
+            st = merge_ranks(ctx, nf, &nf);
+            if (st != MIST_OK) return st;
+            if (want_fp) {
+                ncclResult_t r = ncclAllReduce(ctx->fp.p, ctx->fp.p, 2 * (size_t)pp.ng, ncclUint64, ncclSum,
+                                               (ncclComm_t)ctx->nccl, ctx->stream);
+                if (r != ncclSuccess) return fail(ctx, MIST_ERR_NCCL, std::string("ncclAllReduce fp: ") + ncclGetErrorString(r));
+            }
+        }
+        // offsets + packed points
+        CK(ensure(ctx->out, sizeof(mist_point_t) * (size_t)std::max<long long>(1, nf) +
+                                sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc out");
+        mist_point_t* d_pts = (mist_point_t*)ctx->out.p;
+        int64_t* d_off = (int64_t*)((char*)ctx->out.p + sizeof(mist_point_t) * (size_t)std::max<long long>(1, nf));
+        CK(frontier_group_offsets(ctx->stream, ctx->cand.group, nf, pp.ng, d_off), "offsets");
+        CK(pack_points(ctx->stream, ctx->cand, nf, d_pts), "pack");
+        ctx->stats.kernel_launches += 2;
+        ev_end(ctx, htot);
+        ctx->stats.d2h_bytes = sizeof(mist_point_t) * (uint64_t)nf + sizeof(int64_t) * ((uint64_t)pp.ng + 1) +
+                               (want_fp ? sizeof(u64) * 2 * (uint64_t)pp.ng : 0);
+        ctx->cache_points.resize((size_t)nf);
+        ctx->cache_offsets.resize((size_t)pp.ng + 1);
+        if (nf > 0)
+            CK(cudaMemcpyAsync(ctx->cache_points.data(), d_pts, sizeof(mist_point_t) * (size_t)nf,
+                               cudaMemcpyDeviceToHost, ctx->stream), "D2H points");
+        CK(cudaMemcpyAsync(ctx->cache_offsets.data(), d_off, sizeof(int64_t) * ((size_t)pp.ng + 1),
+                           cudaMemcpyDeviceToHost, ctx->stream), "D2H offsets");
+        if (want_fp) {
+            ctx->cache_fp.resize(2 * (size_t)pp.ng);
+            CK(cudaMemcpyAsync(ctx->cache_fp.data(), ctx->fp.p, sizeof(u64) * 2 * (size_t)pp.ng,
+                               cudaMemcpyDeviceToHost, ctx->stream), "D2H fp");
+        }
+        CK(cudaStreamSynchronize(ctx->stream), "final sync");
+        ev_flush(ctx);
+        ctx->cache_key = key;
+        ctx->cache_valid = 1;
+    }
+    const int64_t nf = (int64_t)ctx->cache_points.size();
+    *n_out = nf;
+    if (out_cap < nf || (!out && nf > 0)) return fail(ctx, MIST_ERR_BUFFER_TOO_SMALL, "out_cap too small");
+    const size_t ng = ctx->cache_offsets.size() - 1;
+    if (nf > 0) CK(cudaMemcpy(out, ctx->cache_points.data(), sizeof(mist_point_t) * (size_t)nf, cudaMemcpyDefault), "copy out");
+    if (group_offsets)
+        CK(cudaMemcpy(group_offsets, ctx->cache_offsets.data(), sizeof(int64_t) * (ng + 1), cudaMemcpyDefault), "copy offsets");
+    if (want_fp) {
+        std::vector<uint64_t> c(ng), hs(ng);
+        for (size_t g = 0; g < ng; ++g) { c[g] = ctx->cache_fp[2 * g]; hs[g] = ctx->cache_fp[2 * g + 1]; }
+        if (fp_count) CK(cudaMemcpy(fp_count, c.data(), sizeof(uint64_t) * ng, cudaMemcpyDefault), "copy fp");
+        if (fp_hash) CK(cudaMemcpy(fp_hash, hs.data(), sizeof(uint64_t) * ng, cudaMemcpyDefault), "copy fp");
+    }
+    ctx->cache_valid = 0;   // the cache only serves a retry after BUFFER_TOO_SMALL
+    return MIST_OK;
+}

@@ -1,0 +1,483 @@
+// mist_eval.cu -- a2..a8: tuple precompute, per-config evaluation, feasibility
+// filter and warp-ballot compaction (sm_100a, FP64 CUDA cores; no tensor
+// cores: nothing here is a dense contraction).
+//
+// Paper: Eq. 4-6 over the overlap schedule template
+// (lines 476-492) with the interference model of Alg. 1 (lines 563-605);
+// memory per Eq. 4's constraint (line 683).  Readings O4-O9 in DESIGN.md.
+//
+// Thread mapping: one thread per OO-run = (tuple, kW, kG, kA); it loops over
+// kO = 0..Q.  t never reads OO (P13), so the stable phases (F, B, B' of every
+// block) are evaluated once per run and only the first-microbatch forward F'
+// and the memory are evaluated per config.  Memory is evaluated as exact
+// integers scaled by D = Q*TP*DP (O9), so feasibility is bit-exact.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "mist_internal.h"
+
+namespace mist {
+
+typedef unsigned long long u64;
+
+// ---------------------------------------------------------------------------
+// a2: tuple precompute
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double coll_time(const DevProblem& P, int kind, double bytes, int gsz,
+                                            int inter) {
+    if (gsz == 1) return 0.0;   // O5: a group of one does not communicate
+    const double c = (kind == kAR) ? 2.0 * (gsz - 1) / gsz : (double)(gsz - 1) / gsz;
+    return c * bytes / P.bw[kind][inter] + P.lat[kind][inter];
+}
+
+__device__ void block_const(const DevProblem& P, BlockConst& bc, int z, int DP, int dp_inter,
+                            double ARtp, double W, double Gr, double O, double A0, double A1,
+                            double Tf, double Tb, int nf, int nb) {
+    const double sw = (z == 3) ? 1.0 / DP : 1.0;   // sigma_w, sigma_g, sigma_o
+    const double sg = (z >= 2) ? 1.0 / DP : 1.0;
+    const double so = (z >= 1) ? 1.0 / DP : 1.0;
+    const double ARf = nf * ARtp, ARb = nb * ARtp;
+    const double AGw = coll_time(P, kAG, W, DP, dp_inter);
+    const double RSg = coll_time(P, kRS, Gr, DP, dp_inter);
+    const double ARg = coll_time(P, kAR, Gr, DP, dp_inter);
+    bc.C_F = Tf + ARf;
+    bc.C_B = Tb + ARb;
+    bc.C_B1 = Tb + ARb + (Tf + ARf);                       // recompute (L17)
+    bc.N_F = (z == 3) ? AGw : 0.0;
+    bc.N_B = ((z == 3) ? AGw : 0.0) + ((z >= 2) ? RSg : 0.0);
+    bc.N_Fp = bc.N_F + ((z == 1 || z == 2) ? AGw : 0.0);   // post-update gather (L12)
+    bc.N_Bp = bc.N_B + ((z == 0) ? ARg : 0.0) + ((z == 1) ? RSg : 0.0);
+    const double qh = P.Q * P.bw_h2d, qd = P.Q * P.bw_d2h;
+    bc.sWh = sw * W / qh; bc.sGh = sg * Gr / qh; bc.sOh = so * O / qh;
+    bc.sWd = sw * W / qd; bc.sGd = sg * Gr / qd; bc.sOd = so * O / qd;
+    bc.sAh = A0 / qh; bc.sAd = A0 / qd;
+    bc.sAh1 = A1 / qh; bc.sAd1 = A1 / qd;
+}
+
+__device__ int find_group_by_tuple(const DevGroup* groups, int ng, u64 T) {
+    int lo = 0, hi = ng - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (groups[mid].tuple_offset <= T) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ void make_tuple(const DevProblem& P, const DevGroup* groups, int ng,
+                           const double* __restrict__ coef, u64 T, TupleConst& o) {
+    const int gi = find_group_by_tuple(groups, ng, T);
+    const DevGroup& G = groups[gi];
+    const u64 local = T - G.tuple_offset;
+    const u64 per_split = (u64)P.nz * (G.l + 1);
+    const int split = (int)(local / per_split);
+    const int rem = (int)(local - (u64)split * per_split);
+    const int z = P.zlev[rem / (G.l + 1)];
+    const int c = rem % (G.l + 1);
+    const int TP = G.tp[split], DP = G.dp[split], b = G.b[split], ti = G.ti[split];
+    const int rows = P.n_b * P.n_tp;
+    const double Tf = coef[0 * rows + ti], Tb = coef[1 * rows + ti];
+    const double Tef = coef[2 * rows + ti], Teb = coef[3 * rows + ti];
+    const double Thf = coef[4 * rows + ti], Thb = coef[5 * rows + ti];
+    const int l = G.l, Q = P.Q;
+    const long long kvd = (long long)P.k * P.h / P.a;
+    const double e = P.e, s = P.s, h = P.h, bb = b;
+    const double Pl = (double)(2LL * P.h * P.h + 2LL * P.h * kvd + (long long)(2 + P.g) * P.h * P.f +
+                               (long long)P.nrm * P.h);            // P_layer (O4)
+    const double Vh = (double)P.V * P.h;                            // P_E = P_H (untied)
+    const double X = e * s * bb * h;                                // boundary activation bytes
+    // TP * A_full, TP * A_bnd, TP * A_H (integers; O4 with dropout-free layers)
+    const double TA_full = e * s * bb * (4.0 * h * TP + 2.0 * h + 2.0 * (double)kvd +
+                                         (2.0 + 2.0 * P.g) * P.f + (1.0 - P.fl) * (double)P.a * s);
+    const double TA_bnd = (double)TP * e * s * bb * h;
+    const double TA_H = (double)TP * e * s * bb * h + 4.0 * s * bb * P.V;
+    const double A_full = TA_full / TP, A_bnd = TA_bnd / TP, A_H = TA_H / TP;
+    const int dp_inter = G.n > 1;
+    const double ARtp = coll_time(P, kAR, X, TP, 0);               // TP groups intra-node
+
+    o.idx_base = T * (u64)P.Q1 * P.Q1 * P.Q1 * P.Q1;
+    o.group = gi; o.first = G.first; o.last = G.last; o.c = c;
+    o.nl0 = (double)(l - c); o.nl1 = (double)c;
+    const int p2p_inter = P.N > 1;
+    const double p2p = X / P.bw[kP2P][p2p_inter] + P.lat[kP2P][p2p_inter];
+    o.t_p2p = (G.last ? 0.0 : p2p) + (G.first ? 0.0 : p2p);
+    const int nl = 2 - P.p;                                          // TP all-reduces per layer
+    block_const(P, o.L, z, DP, dp_inter, ARtp, e * Pl / TP, e * Pl / TP, 12.0 * Pl / TP, A_full,
+                A_bnd, Tf, Tb, nl, nl);
+    if (G.first)
+        block_const(P, o.E, z, DP, dp_inter, ARtp, e * Vh / TP, e * Vh / TP, 12.0 * Vh / TP, 0.0, 0.0,
+                    Tef, Teb, 1, 0);
+    if (G.last)
+        block_const(P, o.H, z, DP, dp_inter, ARtp, e * Vh / TP, e * Vh / TP, 12.0 * Vh / TP, A_H, A_H,
+                    Thf, Thb, 0, 1);
+
+    // O9, scaled by D = Q*TP*DP.  All non-negative integers; exact below 2^53.
+    const double sw_ = (z == 3) ? 1.0 : DP, sg_ = (z >= 2) ? 1.0 : DP, so_ = (z >= 1) ? 1.0 : DP;
+    const double Praw = (double)l * Pl + (G.first ? Vh : 0.0) + (G.last ? Vh : 0.0);  // TP * P_st
+    const double m2 = (double)min(l, 2);
+    o.mW = 2.0 * Praw * sw_;
+    o.mG = 2.0 * Praw * sg_;
+    o.mO = 12.0 * Praw * so_;
+    const double lay = m2 * e * Pl * DP;
+    o.wb_c = (z == 3) ? lay * Q : 0.0;  o.wb_k = (z == 3) ? 0.0 : lay;
+    o.gb_c = (z >= 2) ? lay * Q : 0.0;  o.gb_k = (z >= 2) ? 0.0 : lay;
+    o.ob_k = m2 * 12.0 * Pl * so_;
+    o.ma_k = (double)G.w * DP * ((double)c * TA_bnd + (double)(l - c) * TA_full +
+                                 (G.last ? TA_H : 0.0));
+    o.DA = (double)Q * DP * TA_full;
+    o.DAx = c > 0 ? o.DA : 0.0;
+    o.D = (double)Q * TP * DP;
+    o.DMB = (double)P.mem_budget * o.D;
+}
+
+__global__ void k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ groups, int ng,
+                                   const double* __restrict__ coef, u64 T0, u64 nT,
+                                   TupleConst* __restrict__ out) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nT; i += (u64)gridDim.x * blockDim.x) {
+        TupleConst tc;
+        make_tuple(P, groups, ng, coef, T0 + i, tc);
+        out[i] = tc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a5: Alg. 1 PredINTF, branch-free per round (at each round at most
+// one subset matches the row's nonzero pattern, so indexing the factor table
+// by the pattern is the literal algorithm).  Channels C, NCCL, H2D, D2H.
+// ---------------------------------------------------------------------------
+template <bool UNIT>
+__device__ __forceinline__ double pred_intf(double x0, double x1, double x2, double x3,
+                                            const double (*F)[4], const double (*IF)[4]) {
+    if (UNIT) return fmax(fmax(x0, x1), fmax(x2, x3));   // unit factors: perfect overlap = max
+    double T = 0.0;
+#pragma unroll
+    for (int round = 0; round < 3; ++round) {
+        const int pat = (x0 != 0.0) | ((x1 != 0.0) << 1) | ((x2 != 0.0) << 2) | ((x3 != 0.0) << 3);
+        if (__popc(pat) < 2) break;
+        const double s0 = x0 * F[pat][0], s1 = x1 * F[pat][1];
+        const double s2 = x2 * F[pat][2], s3 = x3 * F[pat][3];
+        const double ov = fmin(fmin((pat & 1) ? s0 : CUDART_INF, (pat & 2) ? s1 : CUDART_INF),
+                               fmin((pat & 4) ? s2 : CUDART_INF, (pat & 8) ? s3 : CUDART_INF));
+        x0 = (pat & 1) ? (s0 - ov) * IF[pat][0] : 0.0;
+        x1 = (pat & 2) ? (s1 - ov) * IF[pat][1] : 0.0;
+        x2 = (pat & 4) ? (s2 - ov) * IF[pat][2] : 0.0;
+        x3 = (pat & 8) ? (s3 - ov) * IF[pat][3] : 0.0;
+        T += ov;
+    }
+    return T + (((x0 + x1) + x2) + x3);
+}
+
+// Per-run state: everything that does not depend on kO.
+struct RunState {
+    double t, dbase;
+    double FpH_L, FpD_L0, FpD_L1;   // F' layer H2D / D2H at kO = 0
+    double FpH_E, FpD_E, FpH_H, FpD_H;
+    double Kf, Kb;                  // D*Mem_fwd / D*Mem_bwd without the (Q-kO), kO terms
+};
+
+template <bool UNIT>
+__device__ __forceinline__ void block_stable(const BlockConst& b, bool r1, double kW, double kG,
+                                             double kA, const double (*F)[4], const double (*IF)[4],
+                                             double& TF, double& TB, double& TBp, double& FpD0) {
+    const double sAh = r1 ? b.sAh1 : b.sAh, sAd = r1 ? b.sAd1 : b.sAd;
+    const double CB = r1 ? b.C_B1 : b.C_B;
+    const double FH = kW * b.sWh, FD = kA * sAd;
+    const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
+    TF = pred_intf<UNIT>(b.C_F, b.N_F, FH, FD, F, IF);                 // F
+    TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, F, IF);                    // B
+    TBp = (b.N_Bp == b.N_B) ? TB : pred_intf<UNIT>(CB, b.N_Bp, BH, BD, F, IF);   // B'
+    FpD0 = FD + kW * b.sWd;
+}
+
+template <bool UNIT>
+__device__ __forceinline__ void eval_run(const TupleConst& tc, double kW, double kG, double kA,
+                                         double Q, const double (*F)[4], const double (*IF)[4],
+                                         RunState& rs) {
+    double t = 0.0, db = 0.0, TF, TB, TBp;
+    rs.FpH_L = kW * tc.L.sWh + kG * tc.L.sGh;
+    rs.FpD_L0 = rs.FpD_L1 = 0.0;
+    if (tc.nl0 > 0.0) {
+        block_stable<UNIT>(tc.L, false, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_L0);
+        t += tc.nl0 * (TF + TB);
+        db += tc.nl0 * ((TBp - TB) - TF);
+    }
+    if (tc.nl1 > 0.0) {
+        block_stable<UNIT>(tc.L, true, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_L1);
+        t += tc.nl1 * (TF + TB);
+        db += tc.nl1 * ((TBp - TB) - TF);
+    }
+    if (tc.first) {
+        block_stable<UNIT>(tc.E, false, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_E);
+        rs.FpH_E = kW * tc.E.sWh + kG * tc.E.sGh;
+        t += TF + TB;
+        db += (TBp - TB) - TF;
+    }
+    if (tc.last) {
+        block_stable<UNIT>(tc.H, false, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_H);
+        rs.FpH_H = kW * tc.H.sWh + kG * tc.H.sGh;
+        t += TF + TB;
+        db += (TBp - TB) - TF;
+    }
+    rs.t = t + tc.t_p2p;
+    rs.dbase = db;
+    // O9 (exact): terms independent of kO
+    const double common = tc.mW * (Q - kW) + tc.mG * (Q - kG) + (tc.wb_c + tc.wb_k * kW) +
+                          tc.ma_k * (Q - kA) + tc.DA;
+    rs.Kf = common;
+    rs.Kb = common + (tc.gb_c + tc.gb_k * kG) + tc.DAx;
+}
+
+// One config of the run: returns d; writes D*mem.
+template <bool UNIT>
+__device__ __forceinline__ double eval_kO(const TupleConst& tc, const RunState& rs, double kO,
+                                          double Q, const double (*F)[4], const double (*IF)[4],
+                                          double& memD) {
+    double ds = rs.dbase;
+    const double H = rs.FpH_L + kO * tc.L.sOh;
+    if (tc.nl0 > 0.0)
+        ds += tc.nl0 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, F, IF);
+    if (tc.nl1 > 0.0)
+        ds += tc.nl1 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, F, IF);
+    if (tc.first)
+        ds += pred_intf<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, F, IF);
+    if (tc.last)
+        ds += pred_intf<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, F, IF);
+    const double qo = Q - kO;
+    const double fwd = rs.Kf + tc.mO * qo + tc.ob_k * kO;   // Mem_fwd: + M_ob
+    const double bwd = rs.Kb + tc.mO * qo;                  // Mem_bwd: + M_gb, recompute buffer
+    memD = fmax(fwd, bwd);
+    return fmax(0.0, ds);                                   // L25: clamp at 0
+}
+
+__device__ __forceinline__ u64 splitmix64(u64 x) {
+    u64 z = x + 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// a3-a8: eval kernel.  MODE 0 = frontier candidates, MODE 1 = dense outputs.
+// ---------------------------------------------------------------------------
+
+constexpr int kEvalThreads = 256;
+
+template <bool UNIT, int MODE>
+__global__ void __launch_bounds__(kEvalThreads)
+k_eval(DevProblem P, EvalArgs A) {
+    extern __shared__ double smem[];
+    double (*sF)[4] = reinterpret_cast<double (*)[4]>(smem);
+    double (*sIF)[4] = reinterpret_cast<double (*)[4]>(smem + 64);
+    TupleConst* sT = reinterpret_cast<TupleConst*>(smem + 128);
+    const int tid = threadIdx.x;
+    if (tid < 64) {
+        sF[tid >> 2][tid & 3] = P.F[tid >> 2][tid & 3];
+        sIF[tid >> 2][tid & 3] = P.IF[tid >> 2][tid & 3];
+    }
+    const double Q = P.Q;
+    const int Q1 = P.Q1;
+    const unsigned lane = tid & 31;
+    for (u64 base = (u64)blockIdx.x * kEvalThreads; base < A.n_runs;
+         base += (u64)gridDim.x * kEvalThreads) {
+        const u64 last = min(base + kEvalThreads, A.n_runs) - 1;
+        const u64 tb0 = base / A.R3, tb1 = last / A.R3;
+        const int ntl = (int)(tb1 - tb0 + 1);
+        __syncthreads();   // previous iteration done with sT
+        {
+            const double* src = reinterpret_cast<const double*>(A.tuples + tb0);
+            double* dst = reinterpret_cast<double*>(sT);
+            const int nw = ntl * (int)(sizeof(TupleConst) / 8);
+            for (int i = tid; i < nw; i += kEvalThreads) dst[i] = __ldg(src + i);
+        }
+        __syncthreads();
+        const u64 u = base + tid;
+        bool has = false;
+        double best_y = CUDART_INF, best_t = 0.0, best_mem = 0.0;
+        u64 best_idx = 0;
+        unsigned grp = 0;
+        u64 fcnt = 0, fhash = 0;
+        if (u < A.n_runs) {
+            const unsigned r0 = (unsigned)(base - tb0 * A.R3) + tid;
+            const unsigned tk = r0 / A.R3;
+            unsigned rem = r0 - tk * A.R3;
+            const unsigned kW = rem / A.Q1sq;
+            rem -= kW * A.Q1sq;
+            const unsigned kG = rem / Q1;
+            const unsigned kA = rem - kG * Q1;
+            const TupleConst& tc = sT[tk];
+            grp = tc.group;
+            RunState rs;
+            eval_run<UNIT>(tc, (double)kW, (double)kG, (double)kA, Q, sF, sIF, rs);
+            const u64 idx0 = tc.idx_base + ((u64)(kW * Q1 + kG) * Q1) * Q1 + kA;
+            double kO = 0.0;
+            for (int k = 0; k < Q1; ++k, kO += 1.0) {
+                const u64 idx = idx0 + (u64)k * Q1;
+                if (MODE == 1 && (idx < A.lo || idx >= A.hi)) continue;
+                double memD;
+                const double d = eval_kO<UNIT>(tc, rs, kO, Q, sF, sIF, memD);
+                const bool feas = memD <= tc.DMB;                   // Eq. 4 constraint, exact
+                if (MODE == 1) {
+                    const u64 o = idx - A.lo;
+                    if (A.t) A.t[o] = rs.t;
+                    if (A.d) A.d[o] = d;
+                    if (A.mem) A.mem[o] = memD / tc.D;
+                    if (A.feas) A.feas[o] = feas;
+                } else if (feas) {
+                    // P13: the whole run shares t; keep its min (y, idx)
+                    const double y = P.ykey ? memD / tc.D : d;
+                    if (y < best_y) {
+                        best_y = y; best_idx = idx; best_mem = memD; has = true;
+                    }
+                    if (A.fp) { fcnt++; fhash += splitmix64(idx); }
+                }
+            }
+            best_t = rs.t;
+            if (has) best_mem = best_mem / tc.D;
+        }
+        if (MODE == 0) {
+            // a8: warp-ballot stream compaction, one atomic per warp
+            const unsigned ball = __ballot_sync(0xffffffffu, has);
+            if (ball) {
+                u64 wbase = 0;
+                if (lane == 0) wbase = atomicAdd(A.cand_count, (u64)__popc(ball));
+                wbase = __shfl_sync(0xffffffffu, wbase, 0);
+                if (has) {
+                    const u64 pos = wbase + __popc(ball & ((1u << lane) - 1));
+                    if ((long long)pos < A.cand.cap) {
+                        A.cand.t[pos] = best_t;
+                        A.cand.y[pos] = best_y;
+                        A.cand.mem[pos] = best_mem;
+                        A.cand.idx[pos] = best_idx;
+                        A.cand.group[pos] = grp;
+                    }
+                }
+            }
+            if (A.fp) {
+                // feasible-set fingerprint, warp-aggregated per group
+                const bool active = fcnt > 0;
+                const unsigned am = __ballot_sync(0xffffffffu, active);
+                if (active) {
+                    const unsigned peers = __match_any_sync(am, grp);
+                    const int leader = __ffs(peers) - 1;
+                    u64 c = fcnt, hsh = fhash;
+                    // sum over peers via shuffles restricted to the peer set
+                    for (unsigned m = peers & ~(1u << leader); m; m &= m - 1) {
+                        const int src = __ffs(m) - 1;
+                        const u64 oc = __shfl_sync(peers, fcnt, src);
+                        const u64 oh = __shfl_sync(peers, fhash, src);
+                        if ((int)lane == leader) { c += oc; hsh += oh; }
+                    }
+                    if ((int)lane == leader) {
+                        atomicAdd(A.fp + 2 * (u64)grp, c);
+                        atomicAdd(A.fp + 2 * (u64)grp + 1, hsh);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Arbitrary index list (test hook): one thread per index, tuple built in registers.
+template <bool UNIT>
+__global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int ng,
+                          const double* __restrict__ coef, const u64* __restrict__ idxs, long long n,
+                          double* t, double* d, double* mem, uint8_t* feas) {
+    __shared__ double sF[16][4], sIF[16][4];
+    if (threadIdx.x < 64) {
+        sF[threadIdx.x >> 2][threadIdx.x & 3] = P.F[threadIdx.x >> 2][threadIdx.x & 3];
+        sIF[threadIdx.x >> 2][threadIdx.x & 3] = P.IF[threadIdx.x >> 2][threadIdx.x & 3];
+    }
+    __syncthreads();
+    const u64 Q1 = P.Q1, R = Q1 * Q1 * Q1 * Q1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const u64 idx = idxs[i];
+        const u64 T = idx / R;
+        u64 r = idx - T * R;
+        const unsigned kA = (unsigned)(r % Q1); r /= Q1;
+        const unsigned kO = (unsigned)(r % Q1); r /= Q1;
+        const unsigned kG = (unsigned)(r % Q1); r /= Q1;
+        const unsigned kW = (unsigned)r;
+        TupleConst tc;
+        make_tuple(P, groups, ng, coef, T, tc);
+        RunState rs;
+        eval_run<UNIT>(tc, kW, kG, kA, (double)P.Q, sF, sIF, rs);
+        double memD;
+        const double dd = eval_kO<UNIT>(tc, rs, (double)kO, (double)P.Q, sF, sIF, memD);
+        if (t) t[i] = rs.t;
+        if (d) d[i] = dd;
+        if (mem) mem[i] = memD / tc.D;
+        if (feas) feas[i] = memD <= tc.DMB;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static int sm_count(int device) {
+    static int cached[64] = {0};
+    if (device < 64 && cached[device]) return cached[device];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    if (device < 64) cached[device] = n;
+    return n;
+}
+
+cudaError_t launch_precompute(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,
+                              int ng, const double* coef, u64 T0, u64 nT, TupleConst* out) {
+    if (nT == 0) return cudaSuccess;
+    const int threads = 128;
+    u64 blocks = (nT + threads - 1) / threads;
+    const u64 cap = (u64)sm_count(device) * 16;
+    if (blocks > cap) blocks = cap;
+    k_tuple_precompute<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, T0, nT, out);
+    return cudaGetLastError();
+}
+
+size_t eval_smem_bytes(const DevProblem& P) {
+    const unsigned R3 = (unsigned)P.Q1 * P.Q1 * P.Q1;
+    const unsigned maxt = (kEvalThreads + R3 - 1) / R3 + 1;
+    return 128 * sizeof(double) + maxt * sizeof(TupleConst);
+}
+
+template <bool UNIT, int MODE>
+static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
+    const size_t smem = eval_smem_bytes(P);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_eval<UNIT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        attr_set = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE>, kEvalThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    u64 blocks = (A.n_runs + kEvalThreads - 1) / kEvalThreads;
+    const u64 cap = (u64)sm_count(device) * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) return cudaSuccess;
+    k_eval<UNIT, MODE><<<(unsigned)blocks, kEvalThreads, smem, st>>>(P, A);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A, int mode) {
+    if (P.unit_factors)
+        return mode ? launch_eval_t<true, 1>(st, device, P, A) : launch_eval_t<true, 0>(st, device, P, A);
+    return mode ? launch_eval_t<false, 1>(st, device, P, A) : launch_eval_t<false, 0>(st, device, P, A);
+}
+
+cudaError_t launch_eval_at(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,
+                           int ng, const double* coef, const u64* idx, long long n, double* t,
+                           double* d, double* mem, uint8_t* feas) {
+    if (n <= 0) return cudaSuccess;
+    const int threads = 128;
+    long long blocks = (n + threads - 1) / threads;
+    const long long cap = (long long)sm_count(device) * 8;
+    if (blocks > cap) blocks = cap;
+    if (P.unit_factors)
+        k_eval_at<true><<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, idx, n, t, d, mem, feas);
+    else
+        k_eval_at<false><<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, idx, n, t, d, mem, feas);
+    return cudaGetLastError();
+}
+
+}  // namespace mist
