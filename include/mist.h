@@ -162,6 +162,14 @@ mist_status_t mist_ctx_set_timing(mist_ctx_t* ctx, int enabled);
  * frontiers over NVLink (ncclAllGather) and returns the merged global
  * frontier on every rank. */
 mist_status_t mist_nccl_unique_id(uint8_t id[MIST_NCCL_ID_BYTES]);
+/* Host-only: the equal contiguous share [t_begin, t_end) of the global tuple
+ * range [0, n_tuples) that `rank` of `world` evaluates when
+ * mist_pareto_frontier is called with t_end == 0 and a communicator
+ * (t_begin = floor(n_tuples*rank/world)).  Every tuple holds (Q+1)^4 configs,
+ * so shares are equal in configs.  INVALID_ARG if rank/world
+ * are out of range. */
+mist_status_t mist_shard_range(uint64_t n_tuples, int rank, int world, uint64_t* t_begin,
+                               uint64_t* t_end);
 mist_status_t mist_ctx_init_comm(mist_ctx_t* ctx, const uint8_t id[MIST_NCCL_ID_BYTES],
                                  int rank, int world);
 

@@ -33,6 +33,7 @@ int coef_row(const mist_coeffs_t*, int, int);
 cudaError_t launch_precompute(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                               u64, u64, TupleConst*);
 cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, int);
+size_t eval_smem_bytes(const DevProblem&, unsigned span);
 cudaError_t launch_eval_at(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                            const u64*, long long, double*, double*, double*, uint8_t*);
 // from mist_frontier.cu
@@ -392,6 +393,7 @@ static mist_status_t dense_eval(mist_ctx_t* ctx, const Prepared& pp, u64 begin, 
         A.tuples = (const TupleConst*)ctx->tuples.p;
         A.n_runs = nT * pp.R3;
         A.R3 = pp.R3; A.Q1sq = pp.Q1sq;
+        A.span = 1;
         A.lo = begin; A.hi = end;
         A.t = t; A.d = d; A.mem = mem; A.feas = feas;
         h = ev_begin(ctx, CAT_EVAL);
@@ -482,6 +484,16 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, 
     mist_status_t st = ensure_cand(ctx, C);
     if (st != MIST_OK) return st;
     C = ctx->cand.cap;
+    // runs per thread: enough threads for ~8 waves of resident warps, the rest looped in-thread
+    unsigned span = 1;
+    {
+        const u64 resident = 148ull * 512;
+        const unsigned q1 = (unsigned)pp.P.Q1;
+        if (total_runs / pp.Q1sq >= 8 * resident && eval_smem_bytes(pp.P, pp.Q1sq) <= 96 * 1024)
+            span = pp.Q1sq;
+        else if (total_runs / q1 >= 8 * resident && eval_smem_bytes(pp.P, q1) <= 96 * 1024)
+            span = q1;
+    }
     const u64 runs_chunk = (u64)C / 4;
     const u64 chunk_T = std::max<u64>(1, runs_chunk / pp.R3);
     CK(ensure(ctx->tuples, sizeof(TupleConst) * std::min<u64>(chunk_T, std::max<u64>(1, te - tb))), "alloc tuples");
@@ -523,6 +535,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, 
         A.tuples = (const TupleConst*)ctx->tuples.p;
         A.n_runs = runs;
         A.R3 = pp.R3; A.Q1sq = pp.Q1sq;
+        A.span = span;
         A.cand = ctx->cand;
         A.cand_count = d_count;
         A.fp = d_fp;
@@ -636,8 +649,10 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         u64 tb = t_begin, te = t_end;
         if (te == 0) {
             if (ctx->nccl && ctx->world > 1) {
-                tb = pp.total_tuples * (u64)ctx->rank / (u64)ctx->world;
-                te = pp.total_tuples * (u64)(ctx->rank + 1) / (u64)ctx->world;
+                uint64_t a = 0, b = 0;
+                mist_shard_range(pp.total_tuples, ctx->rank, ctx->world, &a, &b);
+                tb = a;
+                te = b;
             } else {
                 tb = 0;
                 te = pp.total_tuples;

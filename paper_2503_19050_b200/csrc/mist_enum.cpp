@@ -234,6 +234,16 @@ extern "C" mist_status_t mist_enumerate_space(const mist_model_t* model, int64_t
     return MIST_OK;
 }
 
+extern "C" mist_status_t mist_shard_range(uint64_t n_tuples, int rank, int world, uint64_t* t_begin,
+                                          uint64_t* t_end) {
+    if (!t_begin || !t_end || world < 1 || rank < 0 || rank >= world) return MIST_ERR_INVALID_ARG;
+    // floor(n*r/w) without overflow: n < 2^64, w <= 2^31
+    const unsigned __int128 n = n_tuples;
+    *t_begin = (uint64_t)(n * (unsigned)rank / (unsigned)world);
+    *t_end = (uint64_t)(n * (unsigned)(rank + 1) / (unsigned)world);
+    return MIST_OK;
+}
+
 extern "C" const char* mist_status_string(mist_status_t st) {
     switch (st) {
         case MIST_OK: return "MIST_OK";

@@ -15,6 +15,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "mist_internal.h"
 
 namespace mist {
@@ -141,27 +143,39 @@ __global__ void k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ gr
 }
 
 // ---------------------------------------------------------------------------
-// a5: Alg. 1 PredINTF, branch-free per round (at each round at most
-// one subset matches the row's nonzero pattern, so indexing the factor table
-// by the pattern is the literal algorithm).  Channels C, NCCL, H2D, D2H.
+// a5: Alg. 1 PredINTF.  At each round at most one subset matches
+// the row's nonzero pattern, so the literal algorithm is "look up
+// the factor row of the current pattern, scale, take the min, update".  The
+// shared-memory table holds {f, g} per (pattern, channel): f = F, g = 1/F for
+// member channels and f = 1, g = 0 for the others, so that non-member
+// channels stay (+-)0 through the update without selects; for the min they
+// are lifted to +inf by patching only the high word (their low word is 0).
+// Channels: x0 = C, x1 = NCCL (G2G), x2 = H2D (C2G), x3 = D2H (G2C).
 // ---------------------------------------------------------------------------
+typedef double2 FGRow[4];
+
 template <bool UNIT>
 __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, double x3,
-                                            const double (*F)[4], const double (*IF)[4]) {
+                                            const FGRow* __restrict__ FG) {
     if (UNIT) return fmax(fmax(x0, x1), fmax(x2, x3));   // unit factors: perfect overlap = max
     double T = 0.0;
 #pragma unroll
     for (int round = 0; round < 3; ++round) {
-        const int pat = (x0 != 0.0) | ((x1 != 0.0) << 1) | ((x2 != 0.0) << 2) | ((x3 != 0.0) << 3);
+        const bool q0 = x0 != 0.0, q1 = x1 != 0.0, q2 = x2 != 0.0, q3 = x3 != 0.0;
+        const int pat = (int)q0 | ((int)q1 << 1) | ((int)q2 << 2) | ((int)q3 << 3);
         if (__popc(pat) < 2) break;
-        const double s0 = x0 * F[pat][0], s1 = x1 * F[pat][1];
-        const double s2 = x2 * F[pat][2], s3 = x3 * F[pat][3];
-        const double ov = fmin(fmin((pat & 1) ? s0 : CUDART_INF, (pat & 2) ? s1 : CUDART_INF),
-                               fmin((pat & 4) ? s2 : CUDART_INF, (pat & 8) ? s3 : CUDART_INF));
-        x0 = (pat & 1) ? (s0 - ov) * IF[pat][0] : 0.0;
-        x1 = (pat & 2) ? (s1 - ov) * IF[pat][1] : 0.0;
-        x2 = (pat & 4) ? (s2 - ov) * IF[pat][2] : 0.0;
-        x3 = (pat & 8) ? (s3 - ov) * IF[pat][3] : 0.0;
+        const double2 a0 = FG[pat][0], a1 = FG[pat][1], a2 = FG[pat][2], a3 = FG[pat][3];
+        const double s0 = x0 * a0.x, s1 = x1 * a1.x, s2 = x2 * a2.x, s3 = x3 * a3.x;
+        // +inf for non-members: their s is +-0 (low word 0), replace the high word
+        const double m0 = __hiloint2double(q0 ? __double2hiint(s0) : 0x7ff00000, __double2loint(s0));
+        const double m1 = __hiloint2double(q1 ? __double2hiint(s1) : 0x7ff00000, __double2loint(s1));
+        const double m2 = __hiloint2double(q2 ? __double2hiint(s2) : 0x7ff00000, __double2loint(s2));
+        const double m3 = __hiloint2double(q3 ? __double2hiint(s3) : 0x7ff00000, __double2loint(s3));
+        const double ov = fmin(fmin(m0, m1), fmin(m2, m3));
+        x0 = (s0 - ov) * a0.y;     // argmin -> exactly 0; non-members -> -0 (g = 0)
+        x1 = (s1 - ov) * a1.y;
+        x2 = (s2 - ov) * a2.y;
+        x3 = (s3 - ov) * a3.y;
         T += ov;
     }
     return T + (((x0 + x1) + x2) + x3);
@@ -175,78 +189,93 @@ struct RunState {
     double Kf, Kb;                  // D*Mem_fwd / D*Mem_bwd without the (Q-kO), kO terms
 };
 
-template <bool UNIT>
-__device__ __forceinline__ void block_stable(const BlockConst& b, bool r1, double kW, double kG,
-                                             double kA, const double (*F)[4], const double (*IF)[4],
-                                             double& TF, double& TB, double& TBp, double& FpD0) {
-    const double sAh = r1 ? b.sAh1 : b.sAh, sAd = r1 ? b.sAd1 : b.sAd;
-    const double CB = r1 ? b.C_B1 : b.C_B;
-    const double FH = kW * b.sWh, FD = kA * sAd;
-    const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
-    TF = pred_intf<UNIT>(b.C_F, b.N_F, FH, FD, F, IF);                 // F
-    TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, F, IF);                    // B
-    TBp = (b.N_Bp == b.N_B) ? TB : pred_intf<UNIT>(CB, b.N_Bp, BH, BD, F, IF);   // B'
-    FpD0 = FD + kW * b.sWd;
-}
-
-template <bool UNIT>
-__device__ __forceinline__ void eval_run(const TupleConst& tc, double kW, double kG, double kA,
-                                         double Q, const double (*F)[4], const double (*IF)[4],
-                                         RunState& rs) {
-    double t = 0.0, db = 0.0, TF, TB, TBp;
-    rs.FpH_L = kW * tc.L.sWh + kG * tc.L.sGh;
-    rs.FpD_L0 = rs.FpD_L1 = 0.0;
-    if (tc.nl0 > 0.0) {
-        block_stable<UNIT>(tc.L, false, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_L0);
-        t += tc.nl0 * (TF + TB);
-        db += tc.nl0 * ((TBp - TB) - TF);
-    }
-    if (tc.nl1 > 0.0) {
-        block_stable<UNIT>(tc.L, true, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_L1);
-        t += tc.nl1 * (TF + TB);
-        db += tc.nl1 * ((TBp - TB) - TF);
-    }
-    if (tc.first) {
-        block_stable<UNIT>(tc.E, false, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_E);
-        rs.FpH_E = kW * tc.E.sWh + kG * tc.E.sGh;
-        t += TF + TB;
-        db += (TBp - TB) - TF;
-    }
-    if (tc.last) {
-        block_stable<UNIT>(tc.H, false, kW, kG, kA, F, IF, TF, TB, TBp, rs.FpD_H);
-        rs.FpH_H = kW * tc.H.sWh + kG * tc.H.sGh;
-        t += TF + TB;
-        db += (TBp - TB) - TF;
-    }
-    rs.t = t + tc.t_p2p;
-    rs.dbase = db;
-    // O9 (exact): terms independent of kO
+// O9 (exact integers): the kO-independent part of D*Mem_fwd and D*Mem_bwd.
+__device__ __forceinline__ void run_memory(const TupleConst& tc, double kW, double kG, double kA, double Q,
+                                           RunState& rs) {
     const double common = tc.mW * (Q - kW) + tc.mG * (Q - kG) + (tc.wb_c + tc.wb_k * kW) +
                           tc.ma_k * (Q - kA) + tc.DA;
     rs.Kf = common;
     rs.Kb = common + (tc.gb_c + tc.gb_k * kG) + tc.DAx;
 }
 
-// One config of the run: returns d; writes D*mem.
-template <bool UNIT>
-__device__ __forceinline__ double eval_kO(const TupleConst& tc, const RunState& rs, double kO,
-                                          double Q, const double (*F)[4], const double (*IF)[4],
-                                          double& memD) {
-    double ds = rs.dbase;
-    const double H = rs.FpH_L + kO * tc.L.sOh;
-    if (tc.nl0 > 0.0)
-        ds += tc.nl0 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, F, IF);
-    if (tc.nl1 > 0.0)
-        ds += tc.nl1 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, F, IF);
-    if (tc.first)
-        ds += pred_intf<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, F, IF);
-    if (tc.last)
-        ds += pred_intf<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, F, IF);
+// D*max(Mem_fwd, Mem_bwd) of config kO of the run (Eq. 4)
+__device__ __forceinline__ double mem_kO(const TupleConst& tc, const RunState& rs, double kO, double Q) {
     const double qo = Q - kO;
     const double fwd = rs.Kf + tc.mO * qo + tc.ob_k * kO;   // Mem_fwd: + M_ob
     const double bwd = rs.Kb + tc.mO * qo;                  // Mem_bwd: + M_gb, recompute buffer
-    memD = fmax(fwd, bwd);
+    return fmax(fwd, bwd);
+}
+
+template <bool UNIT>
+__device__ __forceinline__ void block_stable(const BlockConst& b, bool r1, double kW, double kG,
+                                             double kA, const FGRow* FG, double& TF, double& TB,
+                                             double& TBp, double& FpD0) {
+    const double sAh = r1 ? b.sAh1 : b.sAh, sAd = r1 ? b.sAd1 : b.sAd;
+    const double CB = r1 ? b.C_B1 : b.C_B;
+    const double FH = kW * b.sWh, FD = kA * sAd;
+    const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
+    TF = pred_intf<UNIT>(b.C_F, b.N_F, FH, FD, FG);                 // F
+    TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, FG);                    // B
+    TBp = (b.N_Bp == b.N_B) ? TB : pred_intf<UNIT>(CB, b.N_Bp, BH, BD, FG);   // B'
+    FpD0 = FD + kW * b.sWd;
+}
+
+// Stable phases of the run: t (Eq. 5) and the kO-independent part of d (Eq. 6).
+template <bool UNIT>
+__device__ __forceinline__ void run_stable(const TupleConst& tc, double kW, double kG, double kA,
+                                           const FGRow* FG, RunState& rs) {
+    double t = 0.0, db = 0.0, TF, TB, TBp;
+    rs.FpH_L = kW * tc.L.sWh + kG * tc.L.sGh;
+    rs.FpD_L0 = rs.FpD_L1 = 0.0;
+    if (tc.nl0 > 0.0) {
+        block_stable<UNIT>(tc.L, false, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_L0);
+        t += tc.nl0 * (TF + TB);
+        db += tc.nl0 * ((TBp - TB) - TF);
+    }
+    if (tc.nl1 > 0.0) {
+        block_stable<UNIT>(tc.L, true, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_L1);
+        t += tc.nl1 * (TF + TB);
+        db += tc.nl1 * ((TBp - TB) - TF);
+    }
+    if (tc.first) {
+        block_stable<UNIT>(tc.E, false, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_E);
+        rs.FpH_E = kW * tc.E.sWh + kG * tc.E.sGh;
+        t += TF + TB;
+        db += (TBp - TB) - TF;
+    }
+    if (tc.last) {
+        block_stable<UNIT>(tc.H, false, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_H);
+        rs.FpH_H = kW * tc.H.sWh + kG * tc.H.sGh;
+        t += TF + TB;
+        db += (TBp - TB) - TF;
+    }
+    rs.t = t + tc.t_p2p;
+    rs.dbase = db;
+}
+
+// d of config kO of the run: first-microbatch forward F' of every block (Eq. 6).
+template <bool UNIT>
+__device__ __forceinline__ double d_kO(const TupleConst& tc, const RunState& rs, double kO, const FGRow* FG) {
+    double ds = rs.dbase;
+    const double H = rs.FpH_L + kO * tc.L.sOh;
+    if (tc.nl0 > 0.0)
+        ds += tc.nl0 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, FG);
+    if (tc.nl1 > 0.0)
+        ds += tc.nl1 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, FG);
+    if (tc.first)
+        ds += pred_intf<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG);
+    if (tc.last)
+        ds += pred_intf<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG);
     return fmax(0.0, ds);                                   // L25: clamp at 0
+}
+
+// fill the {f, g} factor table (non-members: f = 1, g = 0)
+__device__ __forceinline__ void load_fg(const DevProblem& P, FGRow* FG, int tid) {
+    if (tid < 64) {
+        const int pat = tid >> 2, j = tid & 3;
+        const bool member = __popc(pat) >= 2 && ((pat >> j) & 1);
+        FG[pat][j] = member ? make_double2(P.F[pat][j], P.IF[pat][j]) : make_double2(1.0, 0.0);
+    }
 }
 
 __device__ __forceinline__ u64 splitmix64(u64 x) {
@@ -262,25 +291,53 @@ __device__ __forceinline__ u64 splitmix64(u64 x) {
 
 constexpr int kEvalThreads = 256;
 
-template <bool UNIT, int MODE>
-__global__ void __launch_bounds__(kEvalThreads)
+// O10 "p beats q" on (x, y, idx)
+__device__ __forceinline__ bool beats(double tp, double yp, u64 ip, double tq, double yq, u64 iq) {
+    return tp <= tq && yp <= yq && (tp < tq || yp < yq || ip < iq);
+}
+
+// a8: warp-ballot stream compaction, one atomic per warp, coalesced SoA stores
+__device__ __forceinline__ void warp_emit(bool emit, double t, double y, double mem, u64 idx, unsigned grp,
+                                          const EvalArgs& A, unsigned lane) {
+    const unsigned ball = __ballot_sync(0xffffffffu, emit);
+    if (!ball) return;
+    u64 wbase = 0;
+    if (lane == 0) wbase = atomicAdd(A.cand_count, (u64)__popc(ball));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (emit) {
+        const u64 pos = wbase + __popc(ball & ((1u << lane) - 1));
+        if ((long long)pos < A.cand.cap) {
+            A.cand.t[pos] = t;
+            A.cand.y[pos] = y;
+            A.cand.mem[pos] = mem;
+            A.cand.idx[pos] = idx;
+            A.cand.group[pos] = grp;
+        }
+    }
+}
+
+// One thread per unit = `span` consecutive OO-runs of one tuple (span = 1,
+// Q+1 or (Q+1)^2: the kA, or kG and kA, loops run inside the thread).  The
+// thread keeps one cached candidate and emits it only when a later run's
+// candidate is incomparable with it; a cached point beaten by another
+// feasible config of the same group is dropped, which is exact (O10).
+template <bool UNIT, int MODE, int MINB>
+__global__ void __launch_bounds__(kEvalThreads, MINB)
 k_eval(DevProblem P, EvalArgs A) {
     extern __shared__ double smem[];
-    double (*sF)[4] = reinterpret_cast<double (*)[4]>(smem);
-    double (*sIF)[4] = reinterpret_cast<double (*)[4]>(smem + 64);
+    FGRow* FG = reinterpret_cast<FGRow*>(smem);                    // 16 x 4 x {f, g}
     TupleConst* sT = reinterpret_cast<TupleConst*>(smem + 128);
     const int tid = threadIdx.x;
-    if (tid < 64) {
-        sF[tid >> 2][tid & 3] = P.F[tid >> 2][tid & 3];
-        sIF[tid >> 2][tid & 3] = P.IF[tid >> 2][tid & 3];
-    }
+    load_fg(P, FG, tid);
     const double Q = P.Q;
     const int Q1 = P.Q1;
     const unsigned lane = tid & 31;
-    for (u64 base = (u64)blockIdx.x * kEvalThreads; base < A.n_runs;
+    const unsigned span = A.span;
+    const u64 n_units = A.n_runs / span;
+    for (u64 base = (u64)blockIdx.x * kEvalThreads; base < n_units;
          base += (u64)gridDim.x * kEvalThreads) {
-        const u64 last = min(base + kEvalThreads, A.n_runs) - 1;
-        const u64 tb0 = base / A.R3, tb1 = last / A.R3;
+        const u64 last_unit = min(base + kEvalThreads, n_units) - 1;
+        const u64 tb0 = base * span / A.R3, tb1 = (last_unit * span + span - 1) / A.R3;
         const int ntl = (int)(tb1 - tb0 + 1);
         __syncthreads();   // previous iteration done with sT
         {
@@ -290,73 +347,86 @@ k_eval(DevProblem P, EvalArgs A) {
             for (int i = tid; i < nw; i += kEvalThreads) dst[i] = __ldg(src + i);
         }
         __syncthreads();
-        const u64 u = base + tid;
-        bool has = false;
-        double best_y = CUDART_INF, best_t = 0.0, best_mem = 0.0;
-        u64 best_idx = 0;
-        unsigned grp = 0;
+        const bool active = base + tid < n_units;
+        // decode the first run of this unit
+        const unsigned r0 = (unsigned)(base * span - tb0 * A.R3) + (unsigned)tid * span;
+        const unsigned tk = active ? r0 / A.R3 : 0;
+        unsigned rem = r0 - tk * A.R3;
+        unsigned kW = rem / A.Q1sq;
+        rem -= kW * A.Q1sq;
+        unsigned kG = rem / Q1;
+        unsigned kA = rem - kG * Q1;
+        const TupleConst& tc = sT[tk];
+        const unsigned grp = tc.group;
+        bool cv = false;                       // cached candidate
+        double ct = 0.0, cy = 0.0, cm = 0.0;
+        u64 ci = 0;
         u64 fcnt = 0, fhash = 0;
-        if (u < A.n_runs) {
-            const unsigned r0 = (unsigned)(base - tb0 * A.R3) + tid;
-            const unsigned tk = r0 / A.R3;
-            unsigned rem = r0 - tk * A.R3;
-            const unsigned kW = rem / A.Q1sq;
-            rem -= kW * A.Q1sq;
-            const unsigned kG = rem / Q1;
-            const unsigned kA = rem - kG * Q1;
-            const TupleConst& tc = sT[tk];
-            grp = tc.group;
-            RunState rs;
-            eval_run<UNIT>(tc, (double)kW, (double)kG, (double)kA, Q, sF, sIF, rs);
-            const u64 idx0 = tc.idx_base + ((u64)(kW * Q1 + kG) * Q1) * Q1 + kA;
-            double kO = 0.0;
-            for (int k = 0; k < Q1; ++k, kO += 1.0) {
-                const u64 idx = idx0 + (u64)k * Q1;
-                if (MODE == 1 && (idx < A.lo || idx >= A.hi)) continue;
-                double memD;
-                const double d = eval_kO<UNIT>(tc, rs, kO, Q, sF, sIF, memD);
-                const bool feas = memD <= tc.DMB;                   // Eq. 4 constraint, exact
+        for (unsigned j = 0; j < span; ++j) {
+            bool emit = false;
+            double et = 0.0, ey = 0.0, em = 0.0;
+            u64 ei = 0;
+            if (active) {
+                const double dkW = kW, dkG = kG, dkA = kA;
+                RunState rs;
+                run_memory(tc, dkW, dkG, dkA, Q, rs);
+                const u64 idx0 = tc.idx_base + ((u64)(kW * Q1 + kG) * Q1) * Q1 + kA;
+                bool has = false;
+                double best_y = CUDART_INF, best_m = 0.0;
+                u64 best_i = 0;
                 if (MODE == 1) {
-                    const u64 o = idx - A.lo;
-                    if (A.t) A.t[o] = rs.t;
-                    if (A.d) A.d[o] = d;
-                    if (A.mem) A.mem[o] = memD / tc.D;
-                    if (A.feas) A.feas[o] = feas;
-                } else if (feas) {
-                    // P13: the whole run shares t; keep its min (y, idx)
-                    const double y = P.ykey ? memD / tc.D : d;
-                    if (y < best_y) {
-                        best_y = y; best_idx = idx; best_mem = memD; has = true;
+                    run_stable<UNIT>(tc, dkW, dkG, dkA, FG, rs);
+                    double kO = 0.0;
+                    for (int k = 0; k < Q1; ++k, kO += 1.0) {
+                        const u64 idx = idx0 + (u64)k * Q1;
+                        if (idx < A.lo || idx >= A.hi) continue;
+                        const double memD = mem_kO(tc, rs, kO, Q);
+                        const u64 o = idx - A.lo;
+                        if (A.t) A.t[o] = rs.t;
+                        if (A.d) A.d[o] = d_kO<UNIT>(tc, rs, kO, FG);
+                        if (A.mem) A.mem[o] = memD / tc.D;
+                        if (A.feas) A.feas[o] = memD <= tc.DMB;
                     }
-                    if (A.fp) { fcnt++; fhash += splitmix64(idx); }
+                } else if (mem_kO(tc, rs, Q, Q) <= tc.DMB) {
+                    // D*mem is non-increasing in kO (O9: P_raw >= min(l,2) P_layer), so the
+                    // feasible configs of a run are a suffix in kO and a run whose kO = Q
+                    // config is over budget has none: its t and d are never needed.
+                    run_stable<UNIT>(tc, dkW, dkG, dkA, FG, rs);
+                    double kO = 0.0;
+                    for (int k = 0; k < Q1; ++k, kO += 1.0) {
+                        const double memD = mem_kO(tc, rs, kO, Q);
+                        if (!(memD <= tc.DMB)) continue;                 // Eq. 4 constraint, exact
+                        const u64 idx = idx0 + (u64)k * Q1;
+                        // P13: the whole run shares t; keep its min (y, idx)
+                        const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, rs, kO, FG);
+                        if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
+                        if (A.fp) { fcnt++; fhash += splitmix64(idx); }
+                    }
+                }
+                if (MODE == 0 && has) {
+                    const double rt = rs.t, rm = best_m / tc.D;
+                    if (!cv) {
+                        cv = true; ct = rt; cy = best_y; cm = rm; ci = best_i;
+                    } else if (beats(ct, cy, ci, rt, best_y, best_i)) {
+                        // new run's best is beaten by the cached point: drop it
+                    } else {
+                        if (!beats(rt, best_y, best_i, ct, cy, ci)) {   // incomparable: emit the cached one
+                            emit = true; et = ct; ey = cy; em = cm; ei = ci;
+                        }
+                        ct = rt; cy = best_y; cm = rm; ci = best_i;
+                    }
                 }
             }
-            best_t = rs.t;
-            if (has) best_mem = best_mem / tc.D;
+            if (MODE == 0 && span > 1) warp_emit(emit, et, ey, em, ei, grp, A, lane);
+            if (++kA == (unsigned)Q1) { kA = 0; if (++kG == (unsigned)Q1) { kG = 0; ++kW; } }
         }
         if (MODE == 0) {
-            // a8: warp-ballot stream compaction, one atomic per warp
-            const unsigned ball = __ballot_sync(0xffffffffu, has);
-            if (ball) {
-                u64 wbase = 0;
-                if (lane == 0) wbase = atomicAdd(A.cand_count, (u64)__popc(ball));
-                wbase = __shfl_sync(0xffffffffu, wbase, 0);
-                if (has) {
-                    const u64 pos = wbase + __popc(ball & ((1u << lane) - 1));
-                    if ((long long)pos < A.cand.cap) {
-                        A.cand.t[pos] = best_t;
-                        A.cand.y[pos] = best_y;
-                        A.cand.mem[pos] = best_mem;
-                        A.cand.idx[pos] = best_idx;
-                        A.cand.group[pos] = grp;
-                    }
-                }
-            }
+            warp_emit(cv, ct, cy, cm, ci, grp, A, lane);
             if (A.fp) {
                 // feasible-set fingerprint, warp-aggregated per group
-                const bool active = fcnt > 0;
-                const unsigned am = __ballot_sync(0xffffffffu, active);
-                if (active) {
+                const bool any = fcnt > 0;
+                const unsigned am = __ballot_sync(0xffffffffu, any);
+                if (any) {
                     const unsigned peers = __match_any_sync(am, grp);
                     const int leader = __ffs(peers) - 1;
                     u64 c = fcnt, hsh = fhash;
@@ -382,11 +452,8 @@ template <bool UNIT>
 __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int ng,
                           const double* __restrict__ coef, const u64* __restrict__ idxs, long long n,
                           double* t, double* d, double* mem, uint8_t* feas) {
-    __shared__ double sF[16][4], sIF[16][4];
-    if (threadIdx.x < 64) {
-        sF[threadIdx.x >> 2][threadIdx.x & 3] = P.F[threadIdx.x >> 2][threadIdx.x & 3];
-        sIF[threadIdx.x >> 2][threadIdx.x & 3] = P.IF[threadIdx.x >> 2][threadIdx.x & 3];
-    }
+    __shared__ FGRow FG[16];
+    load_fg(P, FG, threadIdx.x);
     __syncthreads();
     const u64 Q1 = P.Q1, R = Q1 * Q1 * Q1 * Q1;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -401,11 +468,11 @@ __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int
         TupleConst tc;
         make_tuple(P, groups, ng, coef, T, tc);
         RunState rs;
-        eval_run<UNIT>(tc, kW, kG, kA, (double)P.Q, sF, sIF, rs);
-        double memD;
-        const double dd = eval_kO<UNIT>(tc, rs, (double)kO, (double)P.Q, sF, sIF, memD);
+        run_memory(tc, kW, kG, kA, (double)P.Q, rs);
+        run_stable<UNIT>(tc, kW, kG, kA, FG, rs);
+        const double memD = mem_kO(tc, rs, (double)kO, (double)P.Q);
         if (t) t[i] = rs.t;
-        if (d) d[i] = dd;
+        if (d) d[i] = d_kO<UNIT>(tc, rs, (double)kO, FG);
         if (mem) mem[i] = memD / tc.D;
         if (feas) feas[i] = memD <= tc.DMB;
     }
@@ -434,35 +501,53 @@ cudaError_t launch_precompute(cudaStream_t st, int device, const DevProblem& P, 
     return cudaGetLastError();
 }
 
-size_t eval_smem_bytes(const DevProblem& P) {
+// shared memory of one eval CTA: factor tables + the tuples its 256 units touch
+size_t eval_smem_bytes(const DevProblem& P, unsigned span) {
     const unsigned R3 = (unsigned)P.Q1 * P.Q1 * P.Q1;
-    const unsigned maxt = (kEvalThreads + R3 - 1) / R3 + 1;
+    const unsigned maxt = (kEvalThreads * span + R3 - 1) / R3 + 1;
     return 128 * sizeof(double) + maxt * sizeof(TupleConst);
 }
 
-template <bool UNIT, int MODE>
+template <bool UNIT, int MODE, int MINB>
 static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
-    const size_t smem = eval_smem_bytes(P);
+    const size_t smem = eval_smem_bytes(P, A.span);
+    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_eval<UNIT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(k_eval<UNIT, MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE>, kEvalThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE, MINB>, kEvalThreads, smem);
     if (per_sm < 1) per_sm = 1;
-    u64 blocks = (A.n_runs + kEvalThreads - 1) / kEvalThreads;
+    const u64 n_units = A.n_runs / A.span;
+    u64 blocks = (n_units + kEvalThreads - 1) / kEvalThreads;
     const u64 cap = (u64)sm_count(device) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) return cudaSuccess;
-    k_eval<UNIT, MODE><<<(unsigned)blocks, kEvalThreads, smem, st>>>(P, A);
+    k_eval<UNIT, MODE, MINB><<<(unsigned)blocks, kEvalThreads, smem, st>>>(P, A);
     return cudaGetLastError();
 }
 
+// CTAs per SM the frontier-mode eval kernel is compiled for (register budget);
+// MIST_EVAL_MINB=2|3 overrides (tuning knob, default measured best).
+static int eval_minb() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("MIST_EVAL_MINB");
+        v = (s && atoi(s) == 3) ? 3 : 2;
+    }
+    return v;
+}
+
 cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A, int mode) {
-    if (P.unit_factors)
-        return mode ? launch_eval_t<true, 1>(st, device, P, A) : launch_eval_t<true, 0>(st, device, P, A);
-    return mode ? launch_eval_t<false, 1>(st, device, P, A) : launch_eval_t<false, 0>(st, device, P, A);
+    const bool m3 = eval_minb() == 3;
+    if (P.unit_factors) {
+        if (mode) return launch_eval_t<true, 1, 2>(st, device, P, A);
+        return m3 ? launch_eval_t<true, 0, 3>(st, device, P, A) : launch_eval_t<true, 0, 2>(st, device, P, A);
+    }
+    if (mode) return launch_eval_t<false, 1, 2>(st, device, P, A);
+    return m3 ? launch_eval_t<false, 0, 3>(st, device, P, A) : launch_eval_t<false, 0, 2>(st, device, P, A);
 }
 
 cudaError_t launch_eval_at(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,

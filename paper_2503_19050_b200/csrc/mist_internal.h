@@ -101,6 +101,7 @@ struct EvalArgs {
     const TupleConst* tuples;   // tuples of the chunk
     unsigned long long n_runs;  // runs in the chunk = nT * Q1^3
     unsigned R3, Q1sq;
+    unsigned span;              // consecutive runs per thread: 1, Q1 or Q1^2 (divides R3)
     CandBuf cand;
     unsigned long long* cand_count;
     unsigned long long* fp;     // [2*n_groups] (count, hash) or null

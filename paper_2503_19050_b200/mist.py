@@ -29,6 +29,7 @@ Y_DELTA, Y_MEM = 0, 1
 
 EXPORTED = ("mist_ctx_create", "mist_ctx_destroy", "mist_status_string", "mist_ctx_last_error",
             "mist_ctx_stats", "mist_ctx_set_timing", "mist_nccl_unique_id", "mist_ctx_init_comm",
+            "mist_shard_range",
             "mist_enumerate_space", "mist_eval_stage_costs", "mist_eval_stage_costs_at",
             "mist_pareto_frontier", "mist_sample_frontier")
 
@@ -106,6 +107,7 @@ def lib():
         L.mist_ctx_set_timing.argtypes = [V, C.c_int]
         L.mist_nccl_unique_id.argtypes = [V]
         L.mist_ctx_init_comm.argtypes = [V, V, C.c_int, C.c_int]
+        L.mist_shard_range.argtypes = [C.c_uint64, C.c_int, C.c_int, P(C.c_uint64), P(C.c_uint64)]
         L.mist_enumerate_space.argtypes = [P(mist_model_t), C.c_int64, P(mist_mesh_t), P(mist_space_t),
                                            P(mist_coeffs_t), P(mist_group_t), C.c_int64, P(C.c_int64),
                                            P(C.c_uint64)]
@@ -250,6 +252,15 @@ def mist_nccl_unique_id() -> bytes:
     if st != 0:
         raise MistError(st, "mist_nccl_unique_id")
     return bytes(buf)
+
+
+def mist_shard_range(n_tuples: int, rank: int, world: int) -> Tuple[int, int]:
+    """This rank's equal contiguous share of the tuple range (host-only)."""
+    a, b = C.c_uint64(0), C.c_uint64(0)
+    st = lib().mist_shard_range(n_tuples, rank, world, C.byref(a), C.byref(b))
+    if st != 0:
+        raise MistError(st, "mist_shard_range")
+    return a.value, b.value
 
 
 def mist_eval_stage_costs(ctx: Context, spec: Spec, begin: int, end: int, t=None, d=None, mem=None,

@@ -1,0 +1,96 @@
+"""N > 1 host-side protocol on CPU (gloo, world_size 2): each rank takes the
+libmist shard of the tuple range (mist_shard_range, the split the NCCL path
+uses), builds its local per-group frontiers, the ranks all-gather them and
+merge with the exact O12 rule -- the result must equal the one-process sweep.
+(The CUDA/NCCL version of the same exchange runs in the -m gpu multi-GPU test.)"""
+import os
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+WORLD = 2
+
+
+def _local_frontier(o, spec, rank, world):
+    from oracle.binding import POINT_DTYPE, frontier_points
+    from paper_2503_19050_b200 import mist
+    tb, te = mist.mist_shard_range(spec.n_tuples, rank, world)
+    R = spec.R
+    lo, hi = tb * R, te * R
+    r = o.eval_range(lo, hi) if hi > lo else dict(t=np.zeros(0), d=np.zeros(0), mem=np.zeros(0),
+                                                   feasible=np.zeros(0, np.uint8))
+    idx = np.arange(lo, hi, dtype=np.uint64)
+    offs = np.array([g.config_offset for g in o.groups] + [o.n_configs], dtype=np.uint64)
+    gid = np.searchsorted(offs, idx, side="right") - 1
+    keep = r["feasible"] == 1
+    pts = np.zeros(int(keep.sum()), dtype=POINT_DTYPE)
+    pts["idx"], pts["t"], pts["y"], pts["mem"], pts["group"] = idx[keep], r["t"][keep], r["d"][keep], \
+        r["mem"][keep], gid[keep]
+    out = [frontier_points(pts[pts["group"] == g], 2) for g in np.unique(pts["group"])]
+    counts = np.bincount(gid[keep], minlength=o.n_groups)
+    return (np.concatenate(out) if out else pts[:0]), counts, (tb, te)
+
+
+def _worker(rank, world, port, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.binding import Oracle, frontier_points
+        from paper_2503_19050_b200 import mist
+        from synth import tiny
+        pb = tiny(4, 4, 1, 4, 8, 2)
+        o, spec = Oracle(pb), mist.Spec(pb)
+        # the 128-byte communicator id travels rank 0 -> all, as in bench.py
+        import torch
+        blob = torch.tensor(list(range(128)) if rank == 0 else [0] * 128, dtype=torch.uint8)
+        dist.broadcast(blob, 0)
+        assert blob.tolist() == list(range(128))
+        local, counts, rng = _local_frontier(o, spec, rank, world)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (local, counts, rng))
+        if rank == 0:
+            ranges = [g[2] for g in gathered]
+            assert ranges[0][0] == 0 and ranges[-1][1] == spec.n_tuples
+            assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+            allp = np.concatenate([g[0] for g in gathered])
+            ref = o.sweep(threads=1)
+            total_counts = sum(g[1] for g in gathered)
+            assert np.array_equal(total_counts, ref["fp_count"])
+            for g in range(o.n_groups):
+                merged = frontier_points(allp[allp["group"] == g], 2)
+                want = ref["points"][ref["offsets"][g]:ref["offsets"][g + 1]]
+                assert merged["idx"].tolist() == want["idx"].tolist()
+            ret.put("ok")
+    except Exception as e:  # pragma: no cover
+        ret.put(repr(e))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_shard_merge():
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, WORLD, port, ret)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert ret.get(timeout=5) == "ok"
+
+
+def test_shard_range_covers_exactly():
+    from paper_2503_19050_b200 import mist
+    for n in (0, 1, 7, 1000, 501492, 27496640):
+        for w in (1, 2, 3, 4, 8):
+            parts = [mist.mist_shard_range(n, r, w) for r in range(w)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(mist.MistError):
+        mist.mist_shard_range(10, 2, 2)
