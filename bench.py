@@ -275,7 +275,8 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
             "stats_last_step": {k: stats[k] for k in ("candidates", "reductions", "sort_keys", "sort_passes",
-                                                     "chunks", "precompute_ms", "reduce_ms", "merge_ms")},
+                                                     "chunks", "precompute_ms", "reduce_ms", "merge_ms",
+                                                     "pilot_ms", "pilot_configs", "rollbacks", "frontier_points")},
             "timed_region_s": region_s,
         }
         print(json.dumps(line), flush=True)

@@ -141,6 +141,9 @@ typedef struct {
     int32_t unit_factors;        /* 1 if the unit-factor (max) specialisation ran */
     uint64_t h2d_bytes;          /* host->device input bytes copied by the call */
     uint64_t d2h_bytes;          /* device->host result bytes copied by the call */
+    double pilot_ms;             /* pilot sub-grid sweeps that seed the staircase filter */
+    uint64_t pilot_configs;      /* configs evaluated by the pilot (extra work, not in configs_evaluated) */
+    int64_t rollbacks;           /* optimistic chunks re-run after a candidate-buffer overflow */
 } mist_stats_t;
 /* total_ms spans the device work of the call from the moment its inputs are
  * resident in HBM to the last kernel (results still on the device). */

@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -33,7 +34,7 @@ int coef_row(const mist_coeffs_t*, int, int);
 cudaError_t launch_precompute(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                               u64, u64, TupleConst*);
 cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, int);
-size_t eval_smem_bytes(const DevProblem&, unsigned span);
+size_t eval_smem_bytes(unsigned R3, unsigned span);
 cudaError_t launch_eval_at(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                            const u64*, long long, double*, double*, double*, uint8_t*);
 // from mist_frontier.cu
@@ -45,7 +46,7 @@ long long scan_tmp_words(long long n);
 // ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
-enum { CAT_EVAL = 0, CAT_PRE = 1, CAT_RED = 2, CAT_MERGE = 3, CAT_TOTAL = 4 };
+enum { CAT_EVAL = 0, CAT_PRE = 1, CAT_RED = 2, CAT_MERGE = 3, CAT_TOTAL = 4, CAT_PILOT = 5 };
 
 static cudaError_t ensure(DevBuf& b, size_t need) {
     if (b.bytes >= need && b.p) return cudaSuccess;
@@ -115,6 +116,7 @@ static void ev_flush(mist_ctx_t* ctx) {
             case CAT_RED: ctx->stats.reduce_ms += ms; break;
             case CAT_MERGE: ctx->stats.merge_ms += ms; break;
             case CAT_TOTAL: ctx->stats.total_ms += ms; break;
+            case CAT_PILOT: ctx->stats.pilot_ms += ms; break;
         }
     }
     ctx->ev_used.clear();
@@ -321,7 +323,7 @@ extern "C" void mist_ctx_destroy(mist_ctx_t* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
     for (DevBuf* b : {&ctx->cand_mem, &ctx->sort_mem, &ctx->tuples, &ctx->scan_tmp, &ctx->groups,
-                      &ctx->coef, &ctx->counters, &ctx->fp, &ctx->xfer, &ctx->out})
+                      &ctx->coef, &ctx->counters, &ctx->fp, &ctx->xfer, &ctx->out, &ctx->foff})
         release(*b);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -475,84 +477,190 @@ static mist_status_t reduce_now(mist_ctx_t* ctx, long long n, long long* nf) {
     return MIST_OK;
 }
 
+// Candidate-buffer bookkeeping of one sweep.  Invariant between launches:
+// the device counter equals `count` (host-known) and count <= C/2, so a
+// frontier_reduce (which needs 2n <= C) is always possible.
+struct SweepCtx {
+    const Prepared* pp = nullptr;
+    u64* d_count = nullptr;
+    u64* d_fp = nullptr;          // [2*ng] or null
+    u64* d_fp_save = nullptr;     // rollback copy
+    int64_t* d_foff = nullptr;    // [ng+1] group offsets of the staircase filter
+    long long C = 0, count = 0;
+    bool filter = false;
+    bool want_fp = false;
+};
+
+static mist_status_t read_count(mist_ctx_t* ctx, SweepCtx& S, long long* out) {
+    u64 c = 0;
+    CK(cudaMemcpyAsync(&c, S.d_count, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream), "read count");
+    CK(cudaStreamSynchronize(ctx->stream), "sync count");
+    *out = (long long)c;
+    return MIST_OK;
+}
+
+static mist_status_t write_count(mist_ctx_t* ctx, SweepCtx& S, long long v) {
+    S.count = v;
+    const u64 c = (u64)v;
+    CK(cudaMemcpyAsync(S.d_count, &c, sizeof(u64), cudaMemcpyHostToDevice, ctx->stream), "set count");
+    CK(cudaStreamSynchronize(ctx->stream), "sync set count");
+    return MIST_OK;
+}
+
+// Reduce the buffer to its exact frontier; the frontier becomes the staircase filter.
+static mist_status_t reduce_buffer(mist_ctx_t* ctx, SweepCtx& S) {
+    long long nf = 0;
+    mist_status_t st = reduce_now(ctx, S.count, &nf);
+    if (st != MIST_OK) return st;
+    st = write_count(ctx, S, nf);
+    if (st != MIST_OK) return st;
+    CK(frontier_group_offsets(ctx->stream, ctx->cand.group, nf, S.pp->ng, S.d_foff), "filter offsets");
+    ctx->stats.kernel_launches += 1;
+    S.filter = nf > 0;
+    return MIST_OK;
+}
+
+// runs per thread: enough units for ~8 waves of resident warps, the rest looped in-thread
+static unsigned choose_span(u64 runs, unsigned radix, unsigned R3) {
+    const u64 resident = 148ull * 512;
+    const unsigned r2 = radix * radix;
+    if (runs / r2 >= 8 * resident && eval_smem_bytes(R3, r2) <= 96 * 1024) return r2;
+    if (runs / radix >= 8 * resident && eval_smem_bytes(R3, radix) <= 96 * 1024) return radix;
+    return 1;
+}
+
+// One optimistic eval launch over chunk-local tuples [t_lo, t_hi) (MODE 0 or 2).
+// If the candidates could overflow C/2, roll back (counter and fingerprints)
+// and split the range in halves, reducing in between.
+static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const TupleConst* tuples, u64 t_lo,
+                              u64 t_hi, unsigned nv, const unsigned* vals) {
+    const Prepared& pp = *S.pp;
+    const unsigned radix = mode == 2 ? nv : (unsigned)pp.P.Q1;
+    const unsigned R3 = radix * radix * radix;
+    const u64 runs = (t_hi - t_lo) * R3;
+    if (S.count > S.C / 4) {                       // keep head-room before launching
+        mist_status_t st = reduce_buffer(ctx, S);
+        if (st != MIST_OK) return st;
+    }
+    const bool safe = (long long)runs + S.count <= S.C / 2;   // cannot overflow even if every run emits
+    if (!safe && mode == 0 && !S.filter) {
+        // no staircase filter: emissions can approach one per run, so do not speculate
+        const u64 piece = std::max<u64>(1, (u64)(S.C / 4) / R3);
+        for (u64 a = t_lo; a < t_hi; a += piece) {
+            mist_status_t st = eval_opt(ctx, S, mode, tuples, a, std::min<u64>(t_hi, a + piece), nv, vals);
+            if (st != MIST_OK) return st;
+        }
+        return MIST_OK;
+    }
+    if (!safe && S.d_fp)
+        CK(cudaMemcpyAsync(S.d_fp_save, S.d_fp, sizeof(u64) * 2 * (size_t)pp.ng, cudaMemcpyDeviceToDevice,
+                           ctx->stream), "save fp");
+    EvalArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.tuples = tuples + t_lo;
+    A.n_runs = runs;
+    A.R3 = R3;
+    A.Q1sq = radix * radix;
+    A.span = choose_span(runs, radix, R3);
+    A.cand = ctx->cand;
+    A.cand_count = S.d_count;
+    A.fp = mode == 0 ? S.d_fp : nullptr;
+    A.nv = nv;
+    for (unsigned i = 0; i < nv && i < 4; ++i) A.vals[i] = vals[i];
+    if (mode == 0 && S.filter) {
+        A.f_t = ctx->cand.t;
+        A.f_y = ctx->cand.y;
+        A.f_idx = ctx->cand.idx;
+        A.f_off = S.d_foff;
+    }
+    const int h = ev_begin(ctx, mode == 2 ? CAT_PILOT : CAT_EVAL);
+    CK(launch_eval(ctx->stream, ctx->device, pp.P, A, mode), "eval");
+    ev_end(ctx, h);
+    ctx->stats.kernel_launches += 1;
+    long long c = 0;
+    mist_status_t st = read_count(ctx, S, &c);
+    if (st != MIST_OK) return st;
+    if (c <= S.C / 2) {
+        S.count = c;
+        return MIST_OK;
+    }
+    // overflow: roll back, then re-run in pieces sized from the observed emission rate
+    ctx->stats.rollbacks++;
+    const long long before = S.count;
+    st = write_count(ctx, S, before);
+    if (st != MIST_OK) return st;
+    if (S.d_fp)
+        CK(cudaMemcpyAsync(S.d_fp, S.d_fp_save, sizeof(u64) * 2 * (size_t)pp.ng, cudaMemcpyDeviceToDevice,
+                           ctx->stream), "restore fp");
+    if (t_hi - t_lo < 2) return fail(ctx, MIST_ERR_OOM, "candidate buffer too small for one tuple");
+    const double per_tuple = (double)(c - before) / (double)(t_hi - t_lo);   // emissions per tuple
+    const double room = (double)(S.C / 4);                                  // after a reduce, at least C/4 free
+    u64 piece = (u64)std::max(1.0, room / std::max(per_tuple, 1e-9) * 0.5);
+    piece = std::min<u64>(piece, (t_hi - t_lo + 1) / 2);
+    for (u64 a = t_lo; a < t_hi; a += piece) {
+        st = eval_opt(ctx, S, mode, tuples, a, std::min<u64>(t_hi, a + piece), nv, vals);
+        if (st != MIST_OK) return st;
+    }
+    return MIST_OK;
+}
+
 static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, bool want_fp,
                            long long* n_front) {
     const u64 total_runs = (te - tb) * pp.R3;
-    // candidate capacity: enough for every run of the range when small, else capped
-    const long long cap_max = 1LL << 27;
-    long long C = std::min<long long>(cap_max, next_pow2((long long)std::min<u64>(total_runs, 1ull << 40) * 2 + 4096));
-    mist_status_t st = ensure_cand(ctx, C);
+    SweepCtx S;
+    S.pp = &pp;
+    S.want_fp = want_fp;
+    // candidate capacity: 2^26 records (2.4 GB + 1 GB sort scratch), less for small ranges
+    S.C = std::min<long long>(1LL << 26, next_pow2((long long)std::min<u64>(total_runs, 1ull << 40) * 2 + 4096));
+    mist_status_t st = ensure_cand(ctx, S.C);
     if (st != MIST_OK) return st;
-    C = ctx->cand.cap;
-    // runs per thread: enough threads for ~8 waves of resident warps, the rest looped in-thread
-    unsigned span = 1;
-    {
-        const u64 resident = 148ull * 512;
-        const unsigned q1 = (unsigned)pp.P.Q1;
-        if (total_runs / pp.Q1sq >= 8 * resident && eval_smem_bytes(pp.P, pp.Q1sq) <= 96 * 1024)
-            span = pp.Q1sq;
-        else if (total_runs / q1 >= 8 * resident && eval_smem_bytes(pp.P, q1) <= 96 * 1024)
-            span = q1;
-    }
-    const u64 runs_chunk = (u64)C / 4;
-    const u64 chunk_T = std::max<u64>(1, runs_chunk / pp.R3);
-    CK(ensure(ctx->tuples, sizeof(TupleConst) * std::min<u64>(chunk_T, std::max<u64>(1, te - tb))), "alloc tuples");
+    S.C = ctx->cand.cap;
+    // tuple table: whole range, at most 4M tuples (2.2 GB) per chunk
+    const u64 chunk_T = std::min<u64>(te - tb, 1ull << 22);
+    CK(ensure(ctx->tuples, sizeof(TupleConst) * chunk_T), "alloc tuples");
     CK(ensure(ctx->counters, 64), "alloc counters");
-    u64* d_count = (u64*)ctx->counters.p;
-    CK(cudaMemsetAsync(d_count, 0, sizeof(u64), ctx->stream), "zero counter");
-    u64* d_fp = nullptr;
+    CK(ensure(ctx->foff, sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc filter offsets");
+    S.d_count = (u64*)ctx->counters.p;
+    S.d_foff = (int64_t*)ctx->foff.p;
+    st = write_count(ctx, S, 0);
+    if (st != MIST_OK) return st;
     if (want_fp) {
-        CK(ensure(ctx->fp, sizeof(u64) * 2 * (size_t)pp.ng), "alloc fp");
-        d_fp = (u64*)ctx->fp.p;
-        CK(cudaMemsetAsync(d_fp, 0, sizeof(u64) * 2 * (size_t)pp.ng, ctx->stream), "zero fp");
+        CK(ensure(ctx->fp, sizeof(u64) * 4 * (size_t)pp.ng), "alloc fp");
+        S.d_fp = (u64*)ctx->fp.p;
+        S.d_fp_save = S.d_fp + 2 * (size_t)pp.ng;
+        CK(cudaMemsetAsync(S.d_fp, 0, sizeof(u64) * 2 * (size_t)pp.ng, ctx->stream), "zero fp");
     }
-    long long known = 0;        // candidates known to be in the buffer (exact after a sync)
-    u64 upper = 0;              // upper bound on the device counter
+    // pilot sub-grid {0, Q/2, Q} (Q >= 8) or {0, Q} on every ratio axis
+    const unsigned Q = (unsigned)pp.P.Q;
+    unsigned vals[4] = {0, Q, 0, 0}, nv = 2;
+    if (Q >= 8) { vals[1] = Q / 2; vals[2] = Q; nv = 3; }
+    const char* env = getenv("MIST_PILOT");
+    const bool pilot = !(env && env[0] == '0') && Q >= 2 && total_runs >= (1ull << 22);
     for (u64 T0 = tb; T0 < te; T0 += chunk_T) {
         const u64 nT = std::min<u64>(chunk_T, te - T0);
-        const u64 runs = nT * pp.R3;
-        if ((long long)(upper + runs) > C / 2) {
-            u64 cnt = 0;
-            CK(cudaMemcpyAsync(&cnt, d_count, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream), "read count");
-            CK(cudaStreamSynchronize(ctx->stream), "sync count");
-            known = (long long)cnt;
-            if ((long long)(cnt + runs) > C / 2) {
-                long long nf = 0;
-                st = reduce_now(ctx, known, &nf);
-                if (st != MIST_OK) return st;
-                known = nf;
-                CK(cudaMemcpyAsync(d_count, &known, sizeof(u64), cudaMemcpyHostToDevice, ctx->stream), "set count");
-                CK(cudaStreamSynchronize(ctx->stream), "sync set count");
-            }
-            upper = (u64)known;
-        }
         int h = ev_begin(ctx, CAT_PRE);
         CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, T0, nT,
                              (TupleConst*)ctx->tuples.p), "precompute");
         ev_end(ctx, h);
-        EvalArgs A;
-        std::memset(&A, 0, sizeof(A));
-        A.tuples = (const TupleConst*)ctx->tuples.p;
-        A.n_runs = runs;
-        A.R3 = pp.R3; A.Q1sq = pp.Q1sq;
-        A.span = span;
-        A.cand = ctx->cand;
-        A.cand_count = d_count;
-        A.fp = d_fp;
-        h = ev_begin(ctx, CAT_EVAL);
-        CK(launch_eval(ctx->stream, ctx->device, pp.P, A, 0), "eval");
-        ev_end(ctx, h);
-        ctx->stats.kernel_launches += 2;
+        ctx->stats.kernel_launches += 1;
+        const TupleConst* tup = (const TupleConst*)ctx->tuples.p;
+        if (pilot) {
+            // a pilot sweep of the sub-grid seeds an exact staircase filter (its points are
+            // real feasible configs of the same groups, so anything they beat is beaten)
+            st = eval_opt(ctx, S, 2, tup, 0, nT, nv, vals);
+            if (st != MIST_OK) return st;
+            st = reduce_buffer(ctx, S);
+            if (st != MIST_OK) return st;
+            ctx->stats.pilot_configs += nT * (u64)nv * nv * nv * nv;
+        }
+        st = eval_opt(ctx, S, 0, tup, 0, nT, 0, vals);
+        if (st != MIST_OK) return st;
         ctx->stats.chunks++;
-        upper += runs;
         maybe_flush(ctx);
     }
-    u64 cnt = 0;
-    CK(cudaMemcpyAsync(&cnt, d_count, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream), "read count");
-    CK(cudaStreamSynchronize(ctx->stream), "sync count");
-    ctx->stats.candidates += cnt;   // includes carried-over frontier points; refined below
+    ctx->stats.candidates += (uint64_t)S.count;   // before the final reduction
     long long nf = 0;
-    st = reduce_now(ctx, (long long)cnt, &nf);
+    st = reduce_now(ctx, S.count, &nf);
     if (st != MIST_OK) return st;
     ctx->stats.configs_evaluated += (te - tb) * pp.R;
     ctx->stats.frontier_points = (uint64_t)nf;

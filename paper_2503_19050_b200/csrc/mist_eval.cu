@@ -148,16 +148,19 @@ __global__ void k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ gr
 // the factor row of the current pattern, scale, take the min, update".  The
 // shared-memory table holds {f, g} per (pattern, channel): f = F, g = 1/F for
 // member channels and f = 1, g = 0 for the others, so that non-member
-// channels stay (+-)0 through the update without selects; for the min they
-// are lifted to +inf by patching only the high word (their low word is 0).
+// channels stay (+-)0 through the update without selects; the min over the
+// members is a predicated compare-and-select chain (DSETP + 2 FSEL each).
 // Channels: x0 = C, x1 = NCCL (G2G), x2 = H2D (C2G), x3 = D2H (G2C).
 // ---------------------------------------------------------------------------
 typedef double2 FGRow[4];
 
+// min/max without fmin/fmax's NaN handling (no NaN can occur here): DSETP + 2 selects
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
 template <bool UNIT>
 __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, double x3,
                                             const FGRow* __restrict__ FG) {
-    if (UNIT) return fmax(fmax(x0, x1), fmax(x2, x3));   // unit factors: perfect overlap = max
+    if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));   // unit factors: perfect overlap = max
     double T = 0.0;
 #pragma unroll
     for (int round = 0; round < 3; ++round) {
@@ -166,12 +169,11 @@ __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, dou
         if (__popc(pat) < 2) break;
         const double2 a0 = FG[pat][0], a1 = FG[pat][1], a2 = FG[pat][2], a3 = FG[pat][3];
         const double s0 = x0 * a0.x, s1 = x1 * a1.x, s2 = x2 * a2.x, s3 = x3 * a3.x;
-        // +inf for non-members: their s is +-0 (low word 0), replace the high word
-        const double m0 = __hiloint2double(q0 ? __double2hiint(s0) : 0x7ff00000, __double2loint(s0));
-        const double m1 = __hiloint2double(q1 ? __double2hiint(s1) : 0x7ff00000, __double2loint(s1));
-        const double m2 = __hiloint2double(q2 ? __double2hiint(s2) : 0x7ff00000, __double2loint(s2));
-        const double m3 = __hiloint2double(q3 ? __double2hiint(s3) : 0x7ff00000, __double2loint(s3));
-        const double ov = fmin(fmin(m0, m1), fmin(m2, m3));
+        // min over the member channels: predicated compare-and-select chain
+        double ov = q0 ? s0 : CUDART_INF;
+        ov = (q1 && s1 < ov) ? s1 : ov;
+        ov = (q2 && s2 < ov) ? s2 : ov;
+        ov = (q3 && s3 < ov) ? s3 : ov;
         x0 = (s0 - ov) * a0.y;     // argmin -> exactly 0; non-members -> -0 (g = 0)
         x1 = (s1 - ov) * a1.y;
         x2 = (s2 - ov) * a2.y;
@@ -203,7 +205,7 @@ __device__ __forceinline__ double mem_kO(const TupleConst& tc, const RunState& r
     const double qo = Q - kO;
     const double fwd = rs.Kf + tc.mO * qo + tc.ob_k * kO;   // Mem_fwd: + M_ob
     const double bwd = rs.Kb + tc.mO * qo;                  // Mem_bwd: + M_gb, recompute buffer
-    return fmax(fwd, bwd);
+    return dmax(fwd, bwd);
 }
 
 template <bool UNIT>
@@ -266,7 +268,7 @@ __device__ __forceinline__ double d_kO(const TupleConst& tc, const RunState& rs,
         ds += pred_intf<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG);
     if (tc.last)
         ds += pred_intf<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG);
-    return fmax(0.0, ds);                                   // L25: clamp at 0
+    return ds > 0.0 ? ds : 0.0;                             // L25: clamp at 0
 }
 
 // fill the {f, g} factor table (non-members: f = 1, g = 0)
@@ -348,14 +350,15 @@ k_eval(DevProblem P, EvalArgs A) {
         }
         __syncthreads();
         const bool active = base + tid < n_units;
-        // decode the first run of this unit
+        // decode the first run of this unit (digits in base `radix`: Q+1, or nv on the pilot sub-grid)
+        const unsigned radix = (MODE == 2) ? A.nv : (unsigned)Q1;
         const unsigned r0 = (unsigned)(base * span - tb0 * A.R3) + (unsigned)tid * span;
         const unsigned tk = active ? r0 / A.R3 : 0;
         unsigned rem = r0 - tk * A.R3;
-        unsigned kW = rem / A.Q1sq;
-        rem -= kW * A.Q1sq;
-        unsigned kG = rem / Q1;
-        unsigned kA = rem - kG * Q1;
+        unsigned iW = rem / A.Q1sq;
+        rem -= iW * A.Q1sq;
+        unsigned iG = rem / radix;
+        unsigned iA = rem - iG * radix;
         const TupleConst& tc = sT[tk];
         const unsigned grp = tc.group;
         bool cv = false;                       // cached candidate
@@ -367,6 +370,9 @@ k_eval(DevProblem P, EvalArgs A) {
             double et = 0.0, ey = 0.0, em = 0.0;
             u64 ei = 0;
             if (active) {
+                const unsigned kW = (MODE == 2) ? A.vals[iW] : iW;
+                const unsigned kG = (MODE == 2) ? A.vals[iG] : iG;
+                const unsigned kA = (MODE == 2) ? A.vals[iA] : iA;
                 const double dkW = kW, dkG = kG, dkA = kA;
                 RunState rs;
                 run_memory(tc, dkW, dkG, dkA, Q, rs);
@@ -392,18 +398,35 @@ k_eval(DevProblem P, EvalArgs A) {
                     // feasible configs of a run are a suffix in kO and a run whose kO = Q
                     // config is over budget has none: its t and d are never needed.
                     run_stable<UNIT>(tc, dkW, dkG, dkA, FG, rs);
-                    double kO = 0.0;
-                    for (int k = 0; k < Q1; ++k, kO += 1.0) {
+                    for (unsigned k = 0; k < radix; ++k) {
+                        const unsigned ko = (MODE == 2) ? A.vals[k] : k;
+                        const double kO = ko;
                         const double memD = mem_kO(tc, rs, kO, Q);
                         if (!(memD <= tc.DMB)) continue;                 // Eq. 4 constraint, exact
-                        const u64 idx = idx0 + (u64)k * Q1;
+                        const u64 idx = idx0 + (u64)ko * Q1;
                         // P13: the whole run shares t; keep its min (y, idx)
                         const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, rs, kO, FG);
                         if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
-                        if (A.fp) { fcnt++; fhash += splitmix64(idx); }
+                        if (MODE == 0 && A.fp) { fcnt++; fhash += splitmix64(idx); }
                     }
                 }
-                if (MODE == 0 && has) {
+                if (MODE == 0 && has && A.f_off) {
+                    // staircase filter: the pilot frontier point with the largest t <= rt has the
+                    // smallest y among all pilot points with t <= rt; if it beats the run's best,
+                    // drop it (exact: it is a real feasible config of the same group, O10)
+                    long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
+                    const double rt = rs.t;
+                    while (lo < hi) {                       // first position with f_t > rt
+                        const long long mid = (lo + hi) >> 1;
+                        if (__ldg(A.f_t + mid) <= rt) lo = mid + 1; else hi = mid;
+                    }
+                    if (lo > A.f_off[grp]) {
+                        const long long k = lo - 1;
+                        if (beats(__ldg(A.f_t + k), __ldg(A.f_y + k), __ldg(A.f_idx + k), rt, best_y, best_i))
+                            has = false;
+                    }
+                }
+                if (MODE != 1 && has) {
                     const double rt = rs.t, rm = best_m / tc.D;
                     if (!cv) {
                         cv = true; ct = rt; cy = best_y; cm = rm; ci = best_i;
@@ -417,10 +440,10 @@ k_eval(DevProblem P, EvalArgs A) {
                     }
                 }
             }
-            if (MODE == 0 && span > 1) warp_emit(emit, et, ey, em, ei, grp, A, lane);
-            if (++kA == (unsigned)Q1) { kA = 0; if (++kG == (unsigned)Q1) { kG = 0; ++kW; } }
+            if (MODE != 1 && span > 1) warp_emit(emit, et, ey, em, ei, grp, A, lane);
+            if (++iA == radix) { iA = 0; if (++iG == radix) { iG = 0; ++iW; } }
         }
-        if (MODE == 0) {
+        if (MODE != 1) {
             warp_emit(cv, ct, cy, cm, ci, grp, A, lane);
             if (A.fp) {
                 // feasible-set fingerprint, warp-aggregated per group
@@ -502,15 +525,14 @@ cudaError_t launch_precompute(cudaStream_t st, int device, const DevProblem& P, 
 }
 
 // shared memory of one eval CTA: factor tables + the tuples its 256 units touch
-size_t eval_smem_bytes(const DevProblem& P, unsigned span) {
-    const unsigned R3 = (unsigned)P.Q1 * P.Q1 * P.Q1;
+size_t eval_smem_bytes(unsigned R3, unsigned span) {
     const unsigned maxt = (kEvalThreads * span + R3 - 1) / R3 + 1;
     return 128 * sizeof(double) + maxt * sizeof(TupleConst);
 }
 
 template <bool UNIT, int MODE, int MINB>
 static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
-    const size_t smem = eval_smem_bytes(P, A.span);
+    const size_t smem = eval_smem_bytes(A.R3, A.span);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {
@@ -543,10 +565,12 @@ static int eval_minb() {
 cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A, int mode) {
     const bool m3 = eval_minb() == 3;
     if (P.unit_factors) {
-        if (mode) return launch_eval_t<true, 1, 2>(st, device, P, A);
+        if (mode == 1) return launch_eval_t<true, 1, 2>(st, device, P, A);
+        if (mode == 2) return launch_eval_t<true, 2, 2>(st, device, P, A);
         return m3 ? launch_eval_t<true, 0, 3>(st, device, P, A) : launch_eval_t<true, 0, 2>(st, device, P, A);
     }
-    if (mode) return launch_eval_t<false, 1, 2>(st, device, P, A);
+    if (mode == 1) return launch_eval_t<false, 1, 2>(st, device, P, A);
+    if (mode == 2) return launch_eval_t<false, 2, 2>(st, device, P, A);
     return m3 ? launch_eval_t<false, 0, 3>(st, device, P, A) : launch_eval_t<false, 0, 2>(st, device, P, A);
 }
 

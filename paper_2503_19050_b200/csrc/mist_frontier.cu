@@ -163,48 +163,74 @@ __global__ void k_radix_upsweep(const u64* __restrict__ t, const u32* __restrict
     block_hist[(long long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-__global__ void k_radix_scatter(const u64* __restrict__ t_in, const u32* __restrict__ g_in,
-                                const u32* __restrict__ v_in, u64* __restrict__ t_out,
-                                u32* __restrict__ g_out, u32* __restrict__ v_out, long long n, int pos,
-                                long long ntiles, const u32* __restrict__ block_off) {
+// Stable scatter of one 2048-key tile: (1) each warp ranks its contiguous
+// 256-key sub-tile with __match_any_sync and warp-private digit counters,
+// (2) one block scan turns per-warp counts into tile-local positions, (3) the
+// tile is reordered by digit in shared memory, (4) threads stream it out so
+// consecutive threads write consecutive addresses of each digit bucket.
+__global__ void __launch_bounds__(kThreads)
+k_radix_scatter(const u64* __restrict__ t_in, const u32* __restrict__ g_in,
+                const u32* __restrict__ v_in, u64* __restrict__ t_out,
+                u32* __restrict__ g_out, u32* __restrict__ v_out, long long n, int pos,
+                long long ntiles, const u32* __restrict__ block_off) {
     constexpr int W = kThreads / 32;
-    __shared__ u32 s_off[256];          // running output offset per digit for this tile
-    __shared__ u32 s_wcnt[W][256];      // per-warp digit counts of the current round
+    __shared__ u32 s_cnt[W][256];        // per-warp digit counts, then per-warp tile offsets
+    __shared__ u32 s_dstart[256];        // tile-local start of each digit bucket
+    __shared__ u32 s_goff[256];          // global start of this tile's part of each bucket
+    __shared__ u32 s_wt[32];
+    __shared__ u64 sk_t[kSortTile];
+    __shared__ u32 sk_g[kSortTile], sk_v[kSortTile];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    s_off[tid] = block_off[(long long)tid * ntiles + blockIdx.x];
-    for (int i = 0; i < W; ++i) s_wcnt[i][tid] = 0;
+    for (int i = 0; i < W; ++i) s_cnt[i][tid] = 0;
+    s_goff[tid] = block_off[(long long)tid * ntiles + blockIdx.x];
     __syncthreads();
     const long long base = (long long)blockIdx.x * kSortTile;
-    for (int j = 0; j < kSortItems; ++j) {
-        const long long i = base + (long long)j * kThreads + tid;
-        const bool valid = i < n;
-        u64 tv = 0; u32 gv = 0, vv = 0, dg = 0xffffffffu;
-        if (valid) {
-            tv = t_in[i]; gv = g_in[i]; vv = v_in[i];
-            dg = digit_of(tv, gv, pos);
-        }
-        const u32 peers = __match_any_sync(0xffffffffu, dg);
-        const u32 rank = __popc(peers & ((1u << lane) - 1));
-        if (valid && rank == 0) s_wcnt[w][dg] = __popc(peers);
-        __syncthreads();
-        {   // thread tid owns digit tid: exclusive scan across warps, advance s_off
-            u32 run = s_off[tid];
+    const long long wbase = base + (long long)w * 32 * kSortItems;
+    u64 tv[kSortItems];
+    u32 gv[kSortItems], vv[kSortItems], dg[kSortItems], rk[kSortItems];
+    const u32 lt = (1u << lane) - 1;
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const u32 c = s_wcnt[k][tid];
-                s_wcnt[k][tid] = run;
-                run += c;
-            }
-            s_off[tid] = run;
+    for (int j = 0; j < kSortItems; ++j) {
+        const long long i = wbase + j * 32 + lane;
+        const bool valid = i < n;
+        tv[j] = valid ? t_in[i] : 0ull;
+        gv[j] = valid ? g_in[i] : 0u;
+        vv[j] = valid ? v_in[i] : 0u;
+        dg[j] = valid ? digit_of(tv[j], gv[j], pos) : 0xffffffffu;
+        const u32 peers = __match_any_sync(0xffffffffu, dg[j]);
+        const u32 before = valid ? s_cnt[w][dg[j]] : 0u;
+        rk[j] = before + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) s_cnt[w][dg[j]] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {   // thread tid owns digit tid: per-warp prefix and the digit's tile total
+        u32 run = 0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const u32 c = s_cnt[k][tid];
+            s_cnt[k][tid] = run;
+            run += c;
         }
-        __syncthreads();
-        if (valid) {
-            const u32 o = s_wcnt[w][dg] + rank;
-            t_out[o] = tv; g_out[o] = gv; v_out[o] = vv;
-        }
-        __syncthreads();
-        for (int k = 0; k < W; ++k) s_wcnt[k][tid] = 0;
-        __syncthreads();
+        u32 total;
+        s_dstart[tid] = block_excl_sum(run, s_wt, total);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        if (dg[j] == 0xffffffffu) continue;
+        const u32 o = s_dstart[dg[j]] + s_cnt[w][dg[j]] + rk[j];
+        sk_t[o] = tv[j]; sk_g[o] = gv[j]; sk_v[o] = vv[j];
+    }
+    __syncthreads();
+    const int tile_n = (int)min((long long)kSortTile, n - base);
+    for (int o = tid; o < tile_n; o += kThreads) {
+        const u64 t = sk_t[o];
+        const u32 g = sk_g[o];
+        const u32 d = digit_of(t, g, pos);
+        const u32 gp = s_goff[d] + (u32)o - s_dstart[d];
+        t_out[gp] = t; g_out[gp] = g; v_out[gp] = sk_v[o];
     }
 }
 

@@ -108,6 +108,15 @@ struct EvalArgs {
     unsigned long long lo, hi;
     double *t, *d, *mem;
     uint8_t* feas;
+    // MODE 2 (pilot): sub-grid of ratio values vals[0..nv) on every axis; R3 = nv^3
+    unsigned nv;
+    unsigned vals[4];
+    // staircase filter (MODE 0): a per-group frontier of real feasible configs
+    // (sorted by t, y strictly decreasing); a candidate beaten by one is dropped
+    const double* f_t;
+    const double* f_y;
+    const unsigned long long* f_idx;
+    const int64_t* f_off;       // [n_groups+1], null = no filter
 };
 
 struct ReduceStats {
@@ -133,7 +142,7 @@ struct mist_ctx {
     std::string last_error;
     mist_stats_t stats{};
     // device scratch (grown on demand, freed by mist_ctx_destroy)
-    mist::DevBuf cand_mem, sort_mem, tuples, scan_tmp, groups, coef, counters, fp, xfer, out;
+    mist::DevBuf cand_mem, sort_mem, tuples, scan_tmp, groups, coef, counters, fp, xfer, out, foff;
     mist::CandBuf cand;            // views into cand_mem
     mist::SortScratch sort;        // views into sort_mem
     // cached last frontier (for BUFFER_TOO_SMALL retries)

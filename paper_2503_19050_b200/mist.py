@@ -80,7 +80,8 @@ class mist_stats_t(C.Structure):
                 ("eval_ms", C.c_double), ("precompute_ms", C.c_double), ("reduce_ms", C.c_double),
                 ("merge_ms", C.c_double), ("total_ms", C.c_double), ("chunks", C.c_int64),
                 ("reductions", C.c_int64), ("sort_keys", C.c_uint64), ("sort_passes", C.c_int32),
-                ("unit_factors", C.c_int32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("unit_factors", C.c_int32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("pilot_ms", C.c_double), ("pilot_configs", C.c_uint64), ("rollbacks", C.c_int64)]
 
 
 POINT_DTYPE = np.dtype([("idx", "<u8"), ("t", "<f8"), ("y", "<f8"), ("mem", "<f8")])
