@@ -34,7 +34,8 @@ int coef_row(const mist_coeffs_t*, int, int);
 cudaError_t launch_precompute(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                               u64, u64, TupleConst*);
 cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, int);
-size_t eval_smem_bytes(unsigned R3, unsigned span);
+size_t eval_smem_bytes(unsigned upt);
+unsigned units_per_tuple(unsigned radix);
 cudaError_t launch_eval_at(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                            const u64*, long long, double*, double*, double*, uint8_t*);
 // from mist_frontier.cu
@@ -393,9 +394,8 @@ static mist_status_t dense_eval(mist_ctx_t* ctx, const Prepared& pp, u64 begin, 
         EvalArgs A;
         std::memset(&A, 0, sizeof(A));
         A.tuples = (const TupleConst*)ctx->tuples.p;
-        A.n_runs = nT * pp.R3;
-        A.R3 = pp.R3; A.Q1sq = pp.Q1sq;
-        A.span = 1;
+        A.upt = units_per_tuple((unsigned)pp.P.Q1);
+        A.n_units = nT * A.upt;
         A.lo = begin; A.hi = end;
         A.t = t; A.d = d; A.mem = mem; A.feas = feas;
         h = ev_begin(ctx, CAT_EVAL);
@@ -520,15 +520,6 @@ static mist_status_t reduce_buffer(mist_ctx_t* ctx, SweepCtx& S) {
     return MIST_OK;
 }
 
-// runs per thread: enough units for ~8 waves of resident warps, the rest looped in-thread
-static unsigned choose_span(u64 runs, unsigned radix, unsigned R3) {
-    const u64 resident = 148ull * 512;
-    const unsigned r2 = radix * radix;
-    if (runs / r2 >= 8 * resident && eval_smem_bytes(R3, r2) <= 96 * 1024) return r2;
-    if (runs / radix >= 8 * resident && eval_smem_bytes(R3, radix) <= 96 * 1024) return radix;
-    return 1;
-}
-
 // One optimistic eval launch over chunk-local tuples [t_lo, t_hi) (MODE 0 or 2).
 // If the candidates could overflow C/2, roll back (counter and fingerprints)
 // and split the range in halves, reducing in between.
@@ -558,10 +549,8 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     EvalArgs A;
     std::memset(&A, 0, sizeof(A));
     A.tuples = tuples + t_lo;
-    A.n_runs = runs;
-    A.R3 = R3;
-    A.Q1sq = radix * radix;
-    A.span = choose_span(runs, radix, R3);
+    A.upt = units_per_tuple(radix);
+    A.n_units = (t_hi - t_lo) * A.upt;
     A.cand = ctx->cand;
     A.cand_count = S.d_count;
     A.fp = mode == 0 ? S.d_fp : nullptr;

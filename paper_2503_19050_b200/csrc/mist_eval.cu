@@ -183,6 +183,18 @@ __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, dou
     return T + (((x0 + x1) + x2) + x3);
 }
 
+// Loop nest of one thread: unit (kW, kA) -> run kG -> config kO.
+// F phases read only (kW, kA) (O6: F = [C, NCCL, kW sWh, kA sAd]), so they are
+// evaluated once per unit; B, B' and t once per run (t never reads OO, P13);
+// F' and the memory once per config.
+
+// Per-unit state: the F phase of every block.
+struct UnitState {
+    double tf;                                  // sum over blocks of count * T(F)
+    double FH_L, FH_E, FH_H;                    // F H2D = kW sWh
+    double FD_L0, FD_L1, FD_E, FD_H;            // F D2H = kA sAd (r = 0 / 1 for layers)
+};
+
 // Per-run state: everything that does not depend on kO.
 struct RunState {
     double t, dbase;
@@ -208,51 +220,71 @@ __device__ __forceinline__ double mem_kO(const TupleConst& tc, const RunState& r
     return dmax(fwd, bwd);
 }
 
+// F phases of the unit
 template <bool UNIT>
-__device__ __forceinline__ void block_stable(const BlockConst& b, bool r1, double kW, double kG,
-                                             double kA, const FGRow* FG, double& TF, double& TB,
-                                             double& TBp, double& FpD0) {
-    const double sAh = r1 ? b.sAh1 : b.sAh, sAd = r1 ? b.sAd1 : b.sAd;
-    const double CB = r1 ? b.C_B1 : b.C_B;
-    const double FH = kW * b.sWh, FD = kA * sAd;
+__device__ __forceinline__ void unit_forward(const TupleConst& tc, double kW, double kA, const FGRow* FG,
+                                             UnitState& us) {
+    double tf = 0.0;
+    us.FH_L = kW * tc.L.sWh;
+    us.FD_L0 = kA * tc.L.sAd;
+    us.FD_L1 = kA * tc.L.sAd1;
+    if (tc.nl0 > 0.0) tf += tc.nl0 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L0, FG);
+    if (tc.nl1 > 0.0) tf += tc.nl1 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L1, FG);
+    if (tc.first) {
+        us.FH_E = kW * tc.E.sWh;
+        us.FD_E = kA * tc.E.sAd;
+        tf += pred_intf<UNIT>(tc.E.C_F, tc.E.N_F, us.FH_E, us.FD_E, FG);
+    }
+    if (tc.last) {
+        us.FH_H = kW * tc.H.sWh;
+        us.FD_H = kA * tc.H.sAd;
+        tf += pred_intf<UNIT>(tc.H.C_F, tc.H.N_F, us.FH_H, us.FD_H, FG);
+    }
+    us.tf = tf;
+}
+
+// B and B' of one block; returns T(B), writes T(B') - T(B)
+template <bool UNIT>
+__device__ __forceinline__ double block_backward(const BlockConst& b, bool r1, double FH, double kG, double kA,
+                                                 const FGRow* FG, double& dBp) {
+    const double sAh = r1 ? b.sAh1 : b.sAh;
+    const double CB = r1 ? b.C_B1 : b.C_B;                   // a checkpointed layer recomputes (L17)
     const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
-    TF = pred_intf<UNIT>(b.C_F, b.N_F, FH, FD, FG);                 // F
-    TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, FG);                    // B
-    TBp = (b.N_Bp == b.N_B) ? TB : pred_intf<UNIT>(CB, b.N_Bp, BH, BD, FG);   // B'
-    FpD0 = FD + kW * b.sWd;
+    const double TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, FG);
+    dBp = (b.N_Bp == b.N_B) ? 0.0 : pred_intf<UNIT>(CB, b.N_Bp, BH, BD, FG) - TB;
+    return TB;
 }
 
 // Stable phases of the run: t (Eq. 5) and the kO-independent part of d (Eq. 6).
 template <bool UNIT>
-__device__ __forceinline__ void run_stable(const TupleConst& tc, double kW, double kG, double kA,
-                                           const FGRow* FG, RunState& rs) {
-    double t = 0.0, db = 0.0, TF, TB, TBp;
-    rs.FpH_L = kW * tc.L.sWh + kG * tc.L.sGh;
-    rs.FpD_L0 = rs.FpD_L1 = 0.0;
+__device__ __forceinline__ void run_backward(const TupleConst& tc, const UnitState& us, double kW, double kG,
+                                             double kA, const FGRow* FG, RunState& rs) {
+    double tb = 0.0, db = 0.0, dBp;
+    rs.FpH_L = us.FH_L + kG * tc.L.sGh;
+    rs.FpD_L0 = us.FD_L0 + kW * tc.L.sWd;
+    rs.FpD_L1 = us.FD_L1 + kW * tc.L.sWd;
     if (tc.nl0 > 0.0) {
-        block_stable<UNIT>(tc.L, false, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_L0);
-        t += tc.nl0 * (TF + TB);
-        db += tc.nl0 * ((TBp - TB) - TF);
+        tb += tc.nl0 * block_backward<UNIT>(tc.L, false, us.FH_L, kG, kA, FG, dBp);
+        db += tc.nl0 * dBp;
     }
     if (tc.nl1 > 0.0) {
-        block_stable<UNIT>(tc.L, true, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_L1);
-        t += tc.nl1 * (TF + TB);
-        db += tc.nl1 * ((TBp - TB) - TF);
+        tb += tc.nl1 * block_backward<UNIT>(tc.L, true, us.FH_L, kG, kA, FG, dBp);
+        db += tc.nl1 * dBp;
     }
     if (tc.first) {
-        block_stable<UNIT>(tc.E, false, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_E);
-        rs.FpH_E = kW * tc.E.sWh + kG * tc.E.sGh;
-        t += TF + TB;
-        db += (TBp - TB) - TF;
+        tb += block_backward<UNIT>(tc.E, false, us.FH_E, kG, kA, FG, dBp);
+        db += dBp;
+        rs.FpH_E = us.FH_E + kG * tc.E.sGh;
+        rs.FpD_E = us.FD_E + kW * tc.E.sWd;
     }
     if (tc.last) {
-        block_stable<UNIT>(tc.H, false, kW, kG, kA, FG, TF, TB, TBp, rs.FpD_H);
-        rs.FpH_H = kW * tc.H.sWh + kG * tc.H.sGh;
-        t += TF + TB;
-        db += (TBp - TB) - TF;
+        tb += block_backward<UNIT>(tc.H, false, us.FH_H, kG, kA, FG, dBp);
+        db += dBp;
+        rs.FpH_H = us.FH_H + kG * tc.H.sGh;
+        rs.FpD_H = us.FD_H + kW * tc.H.sWd;
     }
-    rs.t = t + tc.t_p2p;
-    rs.dbase = db;
+    rs.t = (us.tf + tb) + tc.t_p2p;
+    rs.dbase = db - us.tf;
 }
 
 // d of config kO of the run: first-microbatch forward F' of every block (Eq. 6).
@@ -318,11 +350,14 @@ __device__ __forceinline__ void warp_emit(bool emit, double t, double y, double 
     }
 }
 
-// One thread per unit = `span` consecutive OO-runs of one tuple (span = 1,
-// Q+1 or (Q+1)^2: the kA, or kG and kA, loops run inside the thread).  The
-// thread keeps one cached candidate and emits it only when a later run's
-// candidate is incomparable with it; a cached point beaten by another
-// feasible config of the same group is dropped, which is exact (O10).
+// One thread per unit = (tuple, kW, kA); it loops over kG (runs) and kO
+// (configs).  Units of one tuple are padded to a multiple of 32 when there are
+// >= 64 of them, so that a warp never straddles two tuples (the phase
+// structure -- c, z, first/last -- is then warp-uniform).  The thread keeps one
+// cached candidate and emits it only when a later run's candidate is
+// incomparable with it; a point beaten by another feasible config of the same
+// group is dropped, which is exact (O10).  MODE 2 (pilot) walks the sub-grid
+// vals[0..nv) on every ratio axis.
 template <bool UNIT, int MODE, int MINB>
 __global__ void __launch_bounds__(kEvalThreads, MINB)
 k_eval(DevProblem P, EvalArgs A) {
@@ -334,12 +369,13 @@ k_eval(DevProblem P, EvalArgs A) {
     const double Q = P.Q;
     const int Q1 = P.Q1;
     const unsigned lane = tid & 31;
-    const unsigned span = A.span;
-    const u64 n_units = A.n_runs / span;
+    const unsigned radix = (MODE == 2) ? A.nv : (unsigned)Q1;
+    const unsigned upt = A.upt;                       // units per tuple (>= radix^2)
+    const u64 n_units = A.n_units;
     for (u64 base = (u64)blockIdx.x * kEvalThreads; base < n_units;
          base += (u64)gridDim.x * kEvalThreads) {
         const u64 last_unit = min(base + kEvalThreads, n_units) - 1;
-        const u64 tb0 = base * span / A.R3, tb1 = (last_unit * span + span - 1) / A.R3;
+        const u64 tb0 = base / upt, tb1 = last_unit / upt;
         const int ntl = (int)(tb1 - tb0 + 1);
         __syncthreads();   // previous iteration done with sT
         {
@@ -349,31 +385,29 @@ k_eval(DevProblem P, EvalArgs A) {
             for (int i = tid; i < nw; i += kEvalThreads) dst[i] = __ldg(src + i);
         }
         __syncthreads();
-        const bool active = base + tid < n_units;
-        // decode the first run of this unit (digits in base `radix`: Q+1, or nv on the pilot sub-grid)
-        const unsigned radix = (MODE == 2) ? A.nv : (unsigned)Q1;
-        const unsigned r0 = (unsigned)(base * span - tb0 * A.R3) + (unsigned)tid * span;
-        const unsigned tk = active ? r0 / A.R3 : 0;
-        unsigned rem = r0 - tk * A.R3;
-        unsigned iW = rem / A.Q1sq;
-        rem -= iW * A.Q1sq;
-        unsigned iG = rem / radix;
-        unsigned iA = rem - iG * radix;
+        const u64 u = base + tid;
+        const unsigned tk = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
+        const unsigned jj = (unsigned)(u - (tb0 + tk) * (u64)upt);
+        const bool active = u < n_units && jj < radix * radix;
+        const unsigned iW = jj / radix, iA = jj - iW * radix;
+        const unsigned kW = (MODE == 2) ? A.vals[active ? iW : 0] : iW;
+        const unsigned kA = (MODE == 2) ? A.vals[active ? iA : 0] : iA;
+        const double dkW = kW, dkA = kA;
         const TupleConst& tc = sT[tk];
         const unsigned grp = tc.group;
+        UnitState us;
+        if (active) unit_forward<UNIT>(tc, dkW, dkA, FG, us);
         bool cv = false;                       // cached candidate
         double ct = 0.0, cy = 0.0, cm = 0.0;
         u64 ci = 0;
         u64 fcnt = 0, fhash = 0;
-        for (unsigned j = 0; j < span; ++j) {
+        for (unsigned ig = 0; ig < radix; ++ig) {
             bool emit = false;
             double et = 0.0, ey = 0.0, em = 0.0;
             u64 ei = 0;
             if (active) {
-                const unsigned kW = (MODE == 2) ? A.vals[iW] : iW;
-                const unsigned kG = (MODE == 2) ? A.vals[iG] : iG;
-                const unsigned kA = (MODE == 2) ? A.vals[iA] : iA;
-                const double dkW = kW, dkG = kG, dkA = kA;
+                const unsigned kG = (MODE == 2) ? A.vals[ig] : ig;
+                const double dkG = kG;
                 RunState rs;
                 run_memory(tc, dkW, dkG, dkA, Q, rs);
                 const u64 idx0 = tc.idx_base + ((u64)(kW * Q1 + kG) * Q1) * Q1 + kA;
@@ -381,7 +415,7 @@ k_eval(DevProblem P, EvalArgs A) {
                 double best_y = CUDART_INF, best_m = 0.0;
                 u64 best_i = 0;
                 if (MODE == 1) {
-                    run_stable<UNIT>(tc, dkW, dkG, dkA, FG, rs);
+                    run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
                     double kO = 0.0;
                     for (int k = 0; k < Q1; ++k, kO += 1.0) {
                         const u64 idx = idx0 + (u64)k * Q1;
@@ -396,8 +430,8 @@ k_eval(DevProblem P, EvalArgs A) {
                 } else if (mem_kO(tc, rs, Q, Q) <= tc.DMB) {
                     // D*mem is non-increasing in kO (O9: P_raw >= min(l,2) P_layer), so the
                     // feasible configs of a run are a suffix in kO and a run whose kO = Q
-                    // config is over budget has none: its t and d are never needed.
-                    run_stable<UNIT>(tc, dkW, dkG, dkA, FG, rs);
+                    // config is over budget has none: its t and d are never needed (R2).
+                    run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
                     for (unsigned k = 0; k < radix; ++k) {
                         const unsigned ko = (MODE == 2) ? A.vals[k] : k;
                         const double kO = ko;
@@ -440,8 +474,7 @@ k_eval(DevProblem P, EvalArgs A) {
                     }
                 }
             }
-            if (MODE != 1 && span > 1) warp_emit(emit, et, ey, em, ei, grp, A, lane);
-            if (++iA == radix) { iA = 0; if (++iG == radix) { iG = 0; ++iW; } }
+            if (MODE != 1) warp_emit(emit, et, ey, em, ei, grp, A, lane);
         }
         if (MODE != 1) {
             warp_emit(cv, ct, cy, cm, ci, grp, A, lane);
@@ -490,9 +523,11 @@ __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int
         const unsigned kW = (unsigned)r;
         TupleConst tc;
         make_tuple(P, groups, ng, coef, T, tc);
+        UnitState us;
         RunState rs;
+        unit_forward<UNIT>(tc, kW, kA, FG, us);
         run_memory(tc, kW, kG, kA, (double)P.Q, rs);
-        run_stable<UNIT>(tc, kW, kG, kA, FG, rs);
+        run_backward<UNIT>(tc, us, kW, kG, kA, FG, rs);
         const double memD = mem_kO(tc, rs, (double)kO, (double)P.Q);
         if (t) t[i] = rs.t;
         if (d) d[i] = d_kO<UNIT>(tc, rs, (double)kO, FG);
@@ -525,14 +560,20 @@ cudaError_t launch_precompute(cudaStream_t st, int device, const DevProblem& P, 
 }
 
 // shared memory of one eval CTA: factor tables + the tuples its 256 units touch
-size_t eval_smem_bytes(unsigned R3, unsigned span) {
-    const unsigned maxt = (kEvalThreads * span + R3 - 1) / R3 + 1;
+size_t eval_smem_bytes(unsigned upt) {
+    const unsigned maxt = (kEvalThreads + upt - 1) / upt + 1;
     return 128 * sizeof(double) + maxt * sizeof(TupleConst);
+}
+
+// units per tuple: radix^2, padded to a multiple of 32 when >= 64 (warp-uniform tuples)
+unsigned units_per_tuple(unsigned radix) {
+    const unsigned r2 = radix * radix;
+    return r2 >= 64 ? (r2 + 31) / 32 * 32 : r2;
 }
 
 template <bool UNIT, int MODE, int MINB>
 static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
-    const size_t smem = eval_smem_bytes(A.R3, A.span);
+    const size_t smem = eval_smem_bytes(A.upt);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {
@@ -542,8 +583,7 @@ static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& 
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE, MINB>, kEvalThreads, smem);
     if (per_sm < 1) per_sm = 1;
-    const u64 n_units = A.n_runs / A.span;
-    u64 blocks = (n_units + kEvalThreads - 1) / kEvalThreads;
+    u64 blocks = (A.n_units + kEvalThreads - 1) / kEvalThreads;
     const u64 cap = (u64)sm_count(device) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) return cudaSuccess;

@@ -99,9 +99,8 @@ struct SortScratch {
 // feasible config -> cand; MODE 1 (dense): t/d/mem/feas for idx in [lo, hi).
 struct EvalArgs {
     const TupleConst* tuples;   // tuples of the chunk
-    unsigned long long n_runs;  // runs in the chunk = nT * Q1^3
-    unsigned R3, Q1sq;
-    unsigned span;              // consecutive runs per thread: 1, Q1 or Q1^2 (divides R3)
+    unsigned long long n_units; // threads of work = tuples * upt
+    unsigned upt;               // units (kW, kA) per tuple, radix^2 padded (units_per_tuple)
     CandBuf cand;
     unsigned long long* cand_count;
     unsigned long long* fp;     // [2*n_groups] (count, hash) or null
