@@ -39,11 +39,13 @@ WORKLOAD_TEXT = {
     4: "cfg4: GPT-3 22B, 32 GPUs, global batch 512, seq 2048, all PP layer-count/mesh groups",
     5: "cfg5: Falcon-40B, 64 GPUs, global batch 1024, seq 2048, 0.02 offload steps",
 }
-# algorithmic FP64 lane-ops per configuration of the hoisted
-# evaluation (stable phases once per OO-run, F' + memory per config):
-# general factors ~ 175 + 460/(Q+1); unit factors (max) ~ 50.
-def alg_ops_per_config(Q: int, unit: bool) -> float:
-    return 50.0 if unit else 175.0 + 460.0 / (Q + 1)
+# SURVEY.md 8(d) per-unit figures: one Alg. 1 phase row costs ~56 FP64 lane-ops
+# branch-free with general factors (~4 channel + ~4 pattern + 3 rounds x 16 + 4
+# final) and ~7 with unit factors (channels + 3 max); the exact O9 memory of a
+# config ~10 (3 FMA, max, compare, per-run share).  The kernel counts the phase
+# rows it evaluates (stats phases_evaluated), so skipped work is not credited.
+def alg_ops(phases: int, configs: int, unit: bool) -> float:
+    return (7.0 if unit else 56.0) * phases + 10.0 * configs
 
 
 # B200 FP64 issue peak derived from unit counts and clock:
@@ -247,7 +249,7 @@ def main():
     if rank == 0:
         # roofline of the dominant kernel (k_eval): algorithmic FP64 ops / eval time (this rank)
         my_configs = stats["configs_evaluated"]
-        ops = alg_ops_per_config(pb.Q, bool(stats["unit_factors"])) * my_configs
+        ops = alg_ops(int(stats["phases_evaluated"]), my_configs, bool(stats["unit_factors"]))
         achieved = ops / (stats["eval_ms"] / 1e3) / 1e12
         peak = FP64_PEAK_OPS / 1e12
         cpu = None
@@ -265,9 +267,11 @@ def main():
             "frontier_points": int(len(pts)),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_eval", "note": "FP64 lane-ops (FMA=1) per SURVEY 8(d) per-config "
-                         "count x configs / CUDA-event time of k_eval; peak = 148 SM x 64 FP64 lanes x "
-                         "1.965 GHz (derived, DESIGN.md Sec. 6)",
+                         "kernel": "k_eval", "note": "FP64 lane-ops (FMA=1): SURVEY 8(d) per-unit figures (56 per "
+                         "Alg. 1 phase row, 7 with unit factors; 10 per config for O9 memory) x the phase rows "
+                         "the kernel counted + configs, / CUDA-event time of k_eval on the ctx stream; peak = "
+                         "148 SM x 64 FP64 lanes x 1.965 GHz (derived, DESIGN.md 4)",
+                         "phases_per_config": int(stats["phases_evaluated"]) / max(1, my_configs),
                          "eval_ms_per_step": stats["eval_ms"], "share_of_step": stats["eval_ms"] / max(1e-9, total_ms_last)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(stats["h2d_bytes"]),

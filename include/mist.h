@@ -144,6 +144,7 @@ typedef struct {
     double pilot_ms;             /* pilot sub-grid sweeps that seed the staircase filter */
     uint64_t pilot_configs;      /* configs evaluated by the pilot (extra work, not in configs_evaluated) */
     int64_t rollbacks;           /* optimistic chunks re-run after a candidate-buffer overflow */
+    uint64_t phases_evaluated;   /* Alg. 1 phase rows (PredINTF calls) the main eval kernel ran */
 } mist_stats_t;
 /* total_ms spans the device work of the call from the moment its inputs are
  * resident in HBM to the last kernel (results still on the device). */
@@ -235,6 +236,20 @@ mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_t* model, i
                                    mist_ykey_t ykey, mist_point_t* out, int64_t out_cap,
                                    int64_t* n_out, int64_t* group_offsets, uint64_t* fp_count,
                                    uint64_t* fp_hash);
+
+/* ---- a9 + a10 on an explicit point set ------------------------------------
+ * Exact per-group frontier (O10 on (x, y) = (t, y), idx tie-break) of the
+ * points points[0..n), point i belonging to group groups[i] (0 <= g < n_groups).
+ * This is the O12 merge step (frontier(A u B) = frontier(frontier(A) u
+ * frontier(B))): e.g. frontiers gathered by other means can be merged here.
+ * points, groups: any memory.  out: any memory, out_cap points, grouped and
+ * t-sorted as in mist_pareto_frontier; group_offsets: any memory, n_groups+1.
+ * Every t must be >= 0 and finite (t orders as its bit pattern).
+ * Errors: INVALID_ARG (n < 0, n_groups < 1 or >= 2^24, group out of range,
+ * negative or non-finite t); BUFFER_TOO_SMALL (*n_out = needed). */
+mist_status_t mist_frontier_points(mist_ctx_t* ctx, const mist_point_t* points, const int32_t* groups,
+                                   int64_t n, int64_t n_groups, mist_point_t* out, int64_t out_cap,
+                                   int64_t* n_out, int64_t* group_offsets);
 
 /* ---- a12: sample_frontier (O11) ----------------------------------
  * Host pointers.  For alpha_j = j/(K-1), j = 0..K-1, picks per group the

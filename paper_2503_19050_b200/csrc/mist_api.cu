@@ -483,6 +483,7 @@ static mist_status_t reduce_now(mist_ctx_t* ctx, long long n, long long* nf) {
 struct SweepCtx {
     const Prepared* pp = nullptr;
     u64* d_count = nullptr;
+    u64* d_phases = nullptr;      // PredINTF-row counter of the main eval kernel
     u64* d_fp = nullptr;          // [2*ng] or null
     u64* d_fp_save = nullptr;     // rollback copy
     int64_t* d_foff = nullptr;    // [ng+1] group offsets of the staircase filter
@@ -554,6 +555,7 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     A.cand = ctx->cand;
     A.cand_count = S.d_count;
     A.fp = mode == 0 ? S.d_fp : nullptr;
+    A.phases = mode == 0 ? S.d_phases : nullptr;
     A.nv = nv;
     for (unsigned i = 0; i < nv && i < 4; ++i) A.vals[i] = vals[i];
     if (mode == 0 && S.filter) {
@@ -610,6 +612,8 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, 
     CK(ensure(ctx->counters, 64), "alloc counters");
     CK(ensure(ctx->foff, sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc filter offsets");
     S.d_count = (u64*)ctx->counters.p;
+    S.d_phases = S.d_count + 1;
+    CK(cudaMemsetAsync(S.d_phases, 0, sizeof(u64), ctx->stream), "zero phase counter");
     S.d_foff = (int64_t*)ctx->foff.p;
     st = write_count(ctx, S, 0);
     if (st != MIST_OK) return st;
@@ -648,6 +652,12 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, 
         maybe_flush(ctx);
     }
     ctx->stats.candidates += (uint64_t)S.count;   // before the final reduction
+    {
+        u64 ph = 0;
+        CK(cudaMemcpyAsync(&ph, S.d_phases, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream), "read phases");
+        CK(cudaStreamSynchronize(ctx->stream), "sync phases");
+        ctx->stats.phases_evaluated += ph;
+    }
     long long nf = 0;
     st = reduce_now(ctx, S.count, &nf);
     if (st != MIST_OK) return st;
@@ -817,5 +827,72 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         if (fp_hash) CK(cudaMemcpy(fp_hash, hs.data(), sizeof(uint64_t) * ng, cudaMemcpyDefault), "copy fp");
     }
     ctx->cache_valid = 0;   // the cache only serves a retry after BUFFER_TOO_SMALL
+    return MIST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// a9 + a10 on an explicit point set (O12 merge)
+// ---------------------------------------------------------------------------
+namespace mist {
+__global__ void k_unpack_points(const mist_point_t* __restrict__ pts, const int32_t* __restrict__ grp, long long n,
+                                int ng, CandBuf c, u32* __restrict__ bad) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const mist_point_t p = pts[i];
+        const int32_t g = grp[i];
+        if (g < 0 || g >= ng || !(p.t >= 0.0) || isinf(p.t)) atomicOr(bad, 1u);
+        c.t[i] = p.t; c.y[i] = p.y; c.mem[i] = p.mem; c.idx[i] = p.idx; c.group[i] = (u32)g;
+    }
+}
+}  // namespace mist
+
+extern "C" mist_status_t mist_frontier_points(mist_ctx_t* ctx, const mist_point_t* points, const int32_t* groups,
+                                              int64_t n, int64_t n_groups, mist_point_t* out, int64_t out_cap,
+                                              int64_t* n_out, int64_t* group_offsets) {
+    if (!ctx || !n_out || n < 0 || n_groups < 1 || n_groups >= (1LL << 24) || (n > 0 && (!points || !groups)))
+        return fail(ctx, MIST_ERR_INVALID_ARG, "bad arguments");
+    CK(cudaSetDevice(ctx->device), "set device");
+    reset_stats(ctx);
+    mist_status_t st = ensure_cand(ctx, next_pow2(2 * n + 4096));
+    if (st != MIST_OK) return st;
+    // stage the inputs on the device (they may be host memory)
+    const size_t pb = sizeof(mist_point_t) * (size_t)std::max<int64_t>(1, n);
+    const size_t gb = sizeof(int32_t) * (size_t)std::max<int64_t>(1, n);
+    CK(ensure(ctx->xfer, pb + gb + 256), "alloc staging");
+    mist_point_t* d_pts = (mist_point_t*)ctx->xfer.p;
+    int32_t* d_grp = (int32_t*)((char*)ctx->xfer.p + pb);
+    CK(ensure(ctx->counters, 64), "alloc counters");
+    u32* d_bad = (u32*)ctx->counters.p;
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(u32), ctx->stream), "zero flag");
+    if (n > 0) {
+        CK(cudaMemcpyAsync(d_pts, points, sizeof(mist_point_t) * (size_t)n, cudaMemcpyDefault, ctx->stream), "stage points");
+        CK(cudaMemcpyAsync(d_grp, groups, sizeof(int32_t) * (size_t)n, cudaMemcpyDefault, ctx->stream), "stage groups");
+        k_unpack_points<<<grid_of(n), 256, 0, ctx->stream>>>(d_pts, d_grp, n, (int)n_groups, ctx->cand, d_bad);
+        ctx->stats.kernel_launches += 1;
+    }
+    u32 bad = 0;
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(u32), cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+    CK(cudaStreamSynchronize(ctx->stream), "sync staging");
+    if (bad) return fail(ctx, MIST_ERR_INVALID_ARG, "group out of range or t negative / non-finite");
+    const int htot = ev_begin(ctx, CAT_TOTAL);
+    long long nf = 0;
+    st = reduce_now(ctx, n, &nf);
+    if (st != MIST_OK) return st;
+    CK(ensure(ctx->out, sizeof(mist_point_t) * (size_t)std::max<long long>(1, nf) +
+                            sizeof(int64_t) * ((size_t)n_groups + 1)), "alloc out");
+    mist_point_t* d_out = (mist_point_t*)ctx->out.p;
+    int64_t* d_off = (int64_t*)((char*)ctx->out.p + sizeof(mist_point_t) * (size_t)std::max<long long>(1, nf));
+    CK(frontier_group_offsets(ctx->stream, ctx->cand.group, nf, (int)n_groups, d_off), "offsets");
+    CK(pack_points(ctx->stream, ctx->cand, nf, d_out), "pack");
+    ctx->stats.kernel_launches += 2;
+    ev_end(ctx, htot);
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    ev_flush(ctx);
+    ctx->stats.frontier_points = (uint64_t)nf;
+    *n_out = nf;
+    if (out_cap < nf || (!out && nf > 0)) return fail(ctx, MIST_ERR_BUFFER_TOO_SMALL, "out_cap too small");
+    if (nf > 0) CK(cudaMemcpy(out, d_out, sizeof(mist_point_t) * (size_t)nf, cudaMemcpyDefault), "copy out");
+    if (group_offsets)
+        CK(cudaMemcpy(group_offsets, d_off, sizeof(int64_t) * ((size_t)n_groups + 1), cudaMemcpyDefault), "copy offsets");
     return MIST_OK;
 }

@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "mist_internal.h"
 
@@ -303,6 +304,34 @@ __device__ __forceinline__ double d_kO(const TupleConst& tc, const RunState& rs,
     return ds > 0.0 ? ds : 0.0;                             // L25: clamp at 0
 }
 
+// Lower bound of d at config kO (R4): Alg. 1 never returns less than the largest
+// channel when every factor is >= 1 (each channel's isolated time is consumed at
+// rate 1/f <= 1 per unit of elapsed overlap), so T(F') >= max(C, NCCL, H2D, D2H).
+// `scale` bounds the magnitudes summed, for a rounding margin.
+__device__ __forceinline__ double d_lower_bound(const TupleConst& tc, const RunState& rs, double kO,
+                                                double& scale) {
+    double lb = rs.dbase, sc = fabs(rs.dbase);
+    const double H = rs.FpH_L + kO * tc.L.sOh;
+    if (tc.nl0 > 0.0) {
+        const double m = dmax(dmax(tc.L.C_F, tc.L.N_Fp), dmax(H, rs.FpD_L0 + kO * tc.L.sOd));
+        lb += tc.nl0 * m; sc += tc.nl0 * m;
+    }
+    if (tc.nl1 > 0.0) {
+        const double m = dmax(dmax(tc.L.C_F, tc.L.N_Fp), dmax(H, rs.FpD_L1 + kO * tc.L.sOd));
+        lb += tc.nl1 * m; sc += tc.nl1 * m;
+    }
+    if (tc.first) {
+        const double m = dmax(dmax(tc.E.C_F, tc.E.N_Fp), dmax(rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd));
+        lb += m; sc += m;
+    }
+    if (tc.last) {
+        const double m = dmax(dmax(tc.H.C_F, tc.H.N_Fp), dmax(rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd));
+        lb += m; sc += m;
+    }
+    scale = sc;
+    return lb;
+}
+
 // fill the {f, g} factor table (non-members: f = 1, g = 0)
 __device__ __forceinline__ void load_fg(const DevProblem& P, FGRow* FG, int tid) {
     if (tid < 64) {
@@ -358,8 +387,8 @@ __device__ __forceinline__ void warp_emit(bool emit, double t, double y, double 
 // incomparable with it; a point beaten by another feasible config of the same
 // group is dropped, which is exact (O10).  MODE 2 (pilot) walks the sub-grid
 // vals[0..nv) on every ratio axis.
-template <bool UNIT, int MODE, int MINB>
-__global__ void __launch_bounds__(kEvalThreads, MINB)
+template <bool UNIT, int MODE, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
 k_eval(DevProblem P, EvalArgs A) {
     extern __shared__ double smem[];
     FGRow* FG = reinterpret_cast<FGRow*>(smem);                    // 16 x 4 x {f, g}
@@ -372,9 +401,9 @@ k_eval(DevProblem P, EvalArgs A) {
     const unsigned radix = (MODE == 2) ? A.nv : (unsigned)Q1;
     const unsigned upt = A.upt;                       // units per tuple (>= radix^2)
     const u64 n_units = A.n_units;
-    for (u64 base = (u64)blockIdx.x * kEvalThreads; base < n_units;
-         base += (u64)gridDim.x * kEvalThreads) {
-        const u64 last_unit = min(base + kEvalThreads, n_units) - 1;
+    for (u64 base = (u64)blockIdx.x * NT; base < n_units;
+         base += (u64)gridDim.x * NT) {
+        const u64 last_unit = min(base + NT, n_units) - 1;
         const u64 tb0 = base / upt, tb1 = last_unit / upt;
         const int ntl = (int)(tb1 - tb0 + 1);
         __syncthreads();   // previous iteration done with sT
@@ -382,7 +411,7 @@ k_eval(DevProblem P, EvalArgs A) {
             const double* src = reinterpret_cast<const double*>(A.tuples + tb0);
             double* dst = reinterpret_cast<double*>(sT);
             const int nw = ntl * (int)(sizeof(TupleConst) / 8);
-            for (int i = tid; i < nw; i += kEvalThreads) dst[i] = __ldg(src + i);
+            for (int i = tid; i < nw; i += NT) dst[i] = __ldg(src + i);
         }
         __syncthreads();
         const u64 u = base + tid;
@@ -397,6 +426,11 @@ k_eval(DevProblem P, EvalArgs A) {
         const unsigned grp = tc.group;
         UnitState us;
         if (active) unit_forward<UNIT>(tc, dkW, dkA, FG, us);
+        // phase rows evaluated by this thread (PredINTF calls), for the roofline's algorithmic count
+        const unsigned nrows = (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
+                               (unsigned)(tc.last != 0);
+        const unsigned brows = nrows * (tc.L.N_Bp != tc.L.N_B ? 2u : 1u);
+        unsigned nph = active ? nrows : 0u;
         bool cv = false;                       // cached candidate
         double ct = 0.0, cy = 0.0, cm = 0.0;
         u64 ci = 0;
@@ -432,16 +466,47 @@ k_eval(DevProblem P, EvalArgs A) {
                     // feasible configs of a run are a suffix in kO and a run whose kO = Q
                     // config is over budget has none: its t and d are never needed (R2).
                     run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
+                    nph += brows;
+                    // Bound-and-skip (ykey = d): a config whose lower bound of d exceeds the
+                    // best d the run already has, or the y of a known feasible point with
+                    // t <= the run's t (pilot staircase / cached candidate, both with a
+                    // smaller-or-unrelated idx, so equal y is not needed), cannot be the run's
+                    // frontier candidate.  The bound is non-decreasing in kO (R4).
+                    double y_thr = CUDART_INF;
+                    if (MODE == 0 && !P.ykey) {
+                        if (cv && ct <= rs.t) y_thr = cy;
+                        if (A.f_off) {
+                            long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
+                            while (lo < hi) {
+                                const long long mid = (lo + hi) >> 1;
+                                if (__ldg(A.f_t + mid) <= rs.t) lo = mid + 1; else hi = mid;
+                            }
+                            if (lo > A.f_off[grp]) {
+                                const double yf = __ldg(A.f_y + lo - 1);
+                                y_thr = yf < y_thr ? yf : y_thr;
+                            }
+                        }
+                    }
                     for (unsigned k = 0; k < radix; ++k) {
                         const unsigned ko = (MODE == 2) ? A.vals[k] : k;
                         const double kO = ko;
                         const double memD = mem_kO(tc, rs, kO, Q);
                         if (!(memD <= tc.DMB)) continue;                 // Eq. 4 constraint, exact
                         const u64 idx = idx0 + (u64)ko * Q1;
+                        if (MODE == 0 && A.fp) { fcnt++; fhash += splitmix64(idx); }
+                        if (MODE == 0 && !P.ykey) {
+                            double scale;
+                            const double lb = d_lower_bound(tc, rs, kO, scale);
+                            const double thr = best_y < y_thr ? best_y : y_thr;
+                            if (lb - 1e-12 * scale > thr) {
+                                if (A.fp) continue;                       // keep counting feasible configs
+                                break;
+                            }
+                        }
                         // P13: the whole run shares t; keep its min (y, idx)
+                        if (!P.ykey) nph += nrows;
                         const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, rs, kO, FG);
                         if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
-                        if (MODE == 0 && A.fp) { fcnt++; fhash += splitmix64(idx); }
                     }
                 }
                 if (MODE == 0 && has && A.f_off) {
@@ -478,6 +543,12 @@ k_eval(DevProblem P, EvalArgs A) {
         }
         if (MODE != 1) {
             warp_emit(cv, ct, cy, cm, ci, grp, A, lane);
+            if (A.phases) {                                   // warp-reduced phase-row count
+                unsigned v = nph;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && v) atomicAdd(A.phases, (u64)v);
+            }
             if (A.fp) {
                 // feasible-set fingerprint, warp-aggregated per group
                 const bool any = fcnt > 0;
@@ -571,47 +642,62 @@ unsigned units_per_tuple(unsigned radix) {
     return r2 >= 64 ? (r2 + 31) / 32 * 32 : r2;
 }
 
-template <bool UNIT, int MODE, int MINB>
+template <bool UNIT, int MODE, int NT, int MINB>
 static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     const size_t smem = eval_smem_bytes(A.upt);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_eval<UNIT, MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_eval<UNIT, MODE, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE, MINB>, kEvalThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE, NT, MINB>, NT, smem);
     if (per_sm < 1) per_sm = 1;
-    u64 blocks = (A.n_units + kEvalThreads - 1) / kEvalThreads;
+    u64 blocks = (A.n_units + NT - 1) / NT;
     const u64 cap = (u64)sm_count(device) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) return cudaSuccess;
-    k_eval<UNIT, MODE, MINB><<<(unsigned)blocks, kEvalThreads, smem, st>>>(P, A);
+    k_eval<UNIT, MODE, NT, MINB><<<(unsigned)blocks, NT, smem, st>>>(P, A);
     return cudaGetLastError();
 }
 
-// CTAs per SM the frontier-mode eval kernel is compiled for (register budget);
-// MIST_EVAL_MINB=2|3 overrides (tuning knob, default measured best).
-static int eval_minb() {
+// CTA shape of the frontier-mode eval kernel: threads x min CTAs per SM (register
+// budget).  MIST_EVAL_CFG = 256x2 | 256x3 | 128x4 | 128x5 | 128x6 (tuning knob).
+static int eval_cfg() {
     static int v = -1;
     if (v < 0) {
-        const char* s = getenv("MIST_EVAL_MINB");
-        v = (s && atoi(s) == 3) ? 3 : 2;
+        const char* s = getenv("MIST_EVAL_CFG");
+        v = 1;   // default 256x3: measured best on cfg2 (profiles/r1, bench_r1i)
+        if (s) {
+            const char* names[5] = {"256x2", "256x3", "128x4", "128x5", "128x6"};
+            for (int i = 0; i < 5; ++i)
+                if (!strcmp(s, names[i])) v = i;
+        }
     }
     return v;
 }
 
-cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A, int mode) {
-    const bool m3 = eval_minb() == 3;
-    if (P.unit_factors) {
-        if (mode == 1) return launch_eval_t<true, 1, 2>(st, device, P, A);
-        if (mode == 2) return launch_eval_t<true, 2, 2>(st, device, P, A);
-        return m3 ? launch_eval_t<true, 0, 3>(st, device, P, A) : launch_eval_t<true, 0, 2>(st, device, P, A);
+template <bool UNIT>
+static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
+    switch (eval_cfg()) {
+        case 1: return launch_eval_t<UNIT, 0, 256, 3>(st, device, P, A);
+        case 2: return launch_eval_t<UNIT, 0, 128, 4>(st, device, P, A);
+        case 3: return launch_eval_t<UNIT, 0, 128, 5>(st, device, P, A);
+        case 4: return launch_eval_t<UNIT, 0, 128, 6>(st, device, P, A);
+        default: return launch_eval_t<UNIT, 0, 256, 2>(st, device, P, A);
     }
-    if (mode == 1) return launch_eval_t<false, 1, 2>(st, device, P, A);
-    if (mode == 2) return launch_eval_t<false, 2, 2>(st, device, P, A);
-    return m3 ? launch_eval_t<false, 0, 3>(st, device, P, A) : launch_eval_t<false, 0, 2>(st, device, P, A);
+}
+
+cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A, int mode) {
+    if (P.unit_factors) {
+        if (mode == 1) return launch_eval_t<true, 1, 256, 2>(st, device, P, A);
+        if (mode == 2) return launch_eval_t<true, 2, 256, 2>(st, device, P, A);
+        return launch_frontier_eval<true>(st, device, P, A);
+    }
+    if (mode == 1) return launch_eval_t<false, 1, 256, 2>(st, device, P, A);
+    if (mode == 2) return launch_eval_t<false, 2, 256, 2>(st, device, P, A);
+    return launch_frontier_eval<false>(st, device, P, A);
 }
 
 cudaError_t launch_eval_at(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,

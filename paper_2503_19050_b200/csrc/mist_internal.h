@@ -104,6 +104,7 @@ struct EvalArgs {
     CandBuf cand;
     unsigned long long* cand_count;
     unsigned long long* fp;     // [2*n_groups] (count, hash) or null
+    unsigned long long* phases; // PredINTF rows evaluated (algorithmic work counter) or null
     unsigned long long lo, hi;
     double *t, *d, *mem;
     uint8_t* feas;

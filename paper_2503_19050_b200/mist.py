@@ -31,7 +31,7 @@ EXPORTED = ("mist_ctx_create", "mist_ctx_destroy", "mist_status_string", "mist_c
             "mist_ctx_stats", "mist_ctx_set_timing", "mist_nccl_unique_id", "mist_ctx_init_comm",
             "mist_shard_range",
             "mist_enumerate_space", "mist_eval_stage_costs", "mist_eval_stage_costs_at",
-            "mist_pareto_frontier", "mist_sample_frontier")
+            "mist_pareto_frontier", "mist_frontier_points", "mist_sample_frontier")
 
 
 class MistError(RuntimeError):
@@ -81,7 +81,8 @@ class mist_stats_t(C.Structure):
                 ("merge_ms", C.c_double), ("total_ms", C.c_double), ("chunks", C.c_int64),
                 ("reductions", C.c_int64), ("sort_keys", C.c_uint64), ("sort_passes", C.c_int32),
                 ("unit_factors", C.c_int32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-                ("pilot_ms", C.c_double), ("pilot_configs", C.c_uint64), ("rollbacks", C.c_int64)]
+                ("pilot_ms", C.c_double), ("pilot_configs", C.c_uint64), ("rollbacks", C.c_int64),
+                ("phases_evaluated", C.c_uint64)]
 
 
 POINT_DTYPE = np.dtype([("idx", "<u8"), ("t", "<f8"), ("y", "<f8"), ("mem", "<f8")])
@@ -120,6 +121,7 @@ def lib():
                                                     P(C.c_int64), V, V, V]
         L.mist_sample_frontier.argtypes = [V, V, C.c_int64, P(mist_group_t), C.c_int32, V, C.c_int64,
                                            P(C.c_int64), V]
+        L.mist_frontier_points.argtypes = [V, V, V, C.c_int64, C.c_int64, V, C.c_int64, P(C.c_int64), V]
         for name in EXPORTED:
             if name not in ("mist_ctx_destroy", "mist_status_string", "mist_ctx_last_error"):
                 getattr(L, name).restype = C.c_int
@@ -308,6 +310,25 @@ def mist_pareto_frontier(ctx: Context, spec: Spec, t_begin: int = 0, t_end: int 
     if isinstance(pts, np.ndarray):
         pts = pts[: n.value]
     return pts, offs, fpc, fph
+
+
+def mist_frontier_points(ctx: Context, points, groups, n_groups: int, out=None, group_offsets=None):
+    """Exact per-group frontier of an explicit point set (O12 merge).
+
+    points: POINT_DTYPE numpy array or a CUDA tensor holding n*4 float64/int64
+    words; groups: int32 numpy array or CUDA tensor.  Returns (points, offsets)."""
+    L = lib()
+    n = len(points) if isinstance(points, np.ndarray) else points.numel() // 4
+    offs = group_offsets if group_offsets is not None else np.zeros(n_groups + 1, dtype=np.int64)
+    cap = n if out is None else (len(out) if isinstance(out, np.ndarray) else out.numel() // 4)
+    res = np.zeros(max(1, cap), dtype=POINT_DTYPE) if out is None else out
+    m = C.c_int64(0)
+    st = L.mist_frontier_points(ctx.handle, _ptr(points), _ptr(groups), n, n_groups, _ptr(res), cap,
+                                C.byref(m), _ptr(offs))
+    ctx.check(st, "mist_frontier_points")
+    if isinstance(res, np.ndarray):
+        res = res[: m.value]
+    return res, offs
 
 
 def mist_sample_frontier(points: np.ndarray, offsets: np.ndarray, spec: Spec, K: int = 16

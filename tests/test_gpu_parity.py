@@ -241,3 +241,34 @@ def test_invalid_groups_rejected(ctx):
     with pytest.raises(mist.MistError) as ei:
         mist.mist_pareto_frontier(ctx, s)
     assert ei.value.status == 1
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_frontier_points_vs_oracle(ctx, seed):
+    """a9 + a10 alone: the GPU radix sort + segmented scan on random point sets
+    (heavy ties in t and y, several digit passes, many groups, ragged sizes)
+    equals the oracle's O(k^2)/sort-scan frontier of the same points, bit for bit."""
+    from oracle.binding import frontier_points as orc_frontier
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300_000)) if seed else 5
+    ng = int(rng.integers(1, 2000))
+    g = np.sort(rng.integers(0, ng, n)).astype(np.int32) if seed % 2 else rng.integers(0, ng, n).astype(np.int32)
+    pts = np.zeros(n, dtype=mist.POINT_DTYPE)
+    if seed % 3 == 0:      # few distinct values: long equal-t runs and y ties
+        pts["t"] = rng.integers(0, 50, n) * 0.125
+        pts["y"] = rng.integers(0, 50, n) * 0.5
+    else:                  # full-precision doubles across many binades
+        pts["t"] = np.exp(rng.uniform(-20, 5, n))
+        pts["y"] = np.exp(rng.uniform(-20, 5, n))
+    pts["idx"] = rng.permutation(n * 4)[:n].astype(np.uint64)
+    pts["mem"] = rng.uniform(0, 1e10, n)
+    fr, offs = mist.mist_frontier_points(ctx, pts, g, ng)
+    for q in range(ng):
+        sel = g == q
+        op = np.zeros(int(sel.sum()), dtype=ORC_POINT)
+        for f in ("idx", "t", "y", "mem"):
+            op[f] = pts[f][sel]
+        want = orc_frontier(op, 2)
+        got = fr[offs[q]:offs[q + 1]]
+        assert got["idx"].tolist() == want["idx"].tolist(), q
+        assert got["t"].tolist() == want["t"].tolist() and got["y"].tolist() == want["y"].tolist()
