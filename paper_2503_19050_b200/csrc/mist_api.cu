@@ -222,7 +222,8 @@ static mist_status_t ensure_cand(mist_ctx_t* ctx, long long C) {
     const long long sort_tiles = (half + 2047) / 2048;
     const size_t cand_bytes = (size_t)C * (8 + 8 + 8 + 8 + 4) + 5 * 256;
     const size_t hist_words = (size_t)std::max<long long>(256 * sort_tiles, half / 16 + 1024) + 256;
-    const size_t sort_bytes = (size_t)half * (8 + 4 + 4) * 2 + hist_words * 4 + 11 * 256 * 4 + 6 * 256;
+    const size_t sort_bytes = (size_t)half * (8 + 4 + 4) * 2 + (size_t)half * 16 + hist_words * 4 + 11 * 256 * 4 +
+                              8 * 256;
     const size_t scan_words = (size_t)scan_tmp_words(std::max<long long>(256 * sort_tiles, half)) + 64;
     release(ctx->cand_mem);
     release(ctx->sort_mem);
@@ -247,6 +248,8 @@ static mist_status_t ensure_cand(mist_ctx_t* ctx, long long C) {
     }
     ctx->sort.block_hist = (u32*)take(4 * hist_words);
     ctx->sort.digit_hist = (u32*)take(4 * 11 * 256);
+    ctx->sort.gy = (double*)take(8 * half);
+    ctx->sort.gidx = (u64*)take(8 * half);
     ctx->sort.cap = half;
     ctx->sort.hist_cap = (long long)hist_words;
     return MIST_OK;

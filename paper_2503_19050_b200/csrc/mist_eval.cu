@@ -379,6 +379,110 @@ __device__ __forceinline__ void warp_emit(bool emit, double t, double y, double 
     }
 }
 
+// Frontier-mode evaluation of one OO-run (tuple, kW, kG, kA): returns the run's
+// candidate = min (d or mem, idx) over its feasible configs, or none.  The
+// staircase filter (pilot frontier) is applied; (cv, ct, cy) is the caller's
+// cached candidate, a known feasible point of the same group.
+struct RunCand {
+    bool has;
+    double t, y, m;
+    u64 idx;
+};
+
+template <bool UNIT, int MODE>
+__device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalArgs& A, const TupleConst& tc,
+                                                const UnitState& us, unsigned kW, unsigned kG, unsigned kA,
+                                                unsigned radix, double Q, int Q1, unsigned grp, const FGRow* FG,
+                                                bool cv, double ct, double cy, unsigned nrows, unsigned brows,
+                                                unsigned& nph, u64& fcnt, u64& fhash) {
+    const double dkW = kW, dkG = kG, dkA = kA;
+    RunState rs;
+    run_memory(tc, dkW, dkG, dkA, Q, rs);
+    rs.t = 0.0;
+    const u64 idx0 = tc.idx_base + ((u64)(kW * Q1 + kG) * Q1) * Q1 + kA;
+    bool has = false;
+    double best_y = CUDART_INF, best_m = 0.0;
+    u64 best_i = 0;
+    if (mem_kO(tc, rs, Q, Q) <= tc.DMB) {
+        // D*mem is non-increasing in kO (O9: P_raw >= min(l,2) P_layer), so the
+        // feasible configs of a run are a suffix in kO and a run whose kO = Q
+        // config is over budget has none: its t and d are never needed (R2).
+        run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
+        nph += brows;
+        // Bound-and-skip (ykey = d): a config whose lower bound of d exceeds the
+        // best d the run already has, or the y of a known feasible point with
+        // t <= the run's t (pilot staircase / cached candidate, both with a
+        // smaller-or-unrelated idx, so equal y is not needed), cannot be the run's
+        // frontier candidate.  The bound is non-decreasing in kO (R4).
+        double y_thr = CUDART_INF;
+        if (MODE == 0 && !P.ykey) {
+            if (cv && ct <= rs.t) y_thr = cy;
+            if (A.f_off) {
+                long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
+                while (lo < hi) {
+                    const long long mid = (lo + hi) >> 1;
+                    if (__ldg(A.f_t + mid) <= rs.t) lo = mid + 1; else hi = mid;
+                }
+                if (lo > A.f_off[grp]) {
+                    const double yf = __ldg(A.f_y + lo - 1);
+                    y_thr = yf < y_thr ? yf : y_thr;
+                }
+            }
+        }
+        // First feasible config of the run: the feasible configs are a suffix in kO
+        // (R2).  Starting every lane's evaluation loop there keeps the warp's F'
+        // evaluations of kO_min in lockstep instead of serialising them.
+        unsigned k0 = 0;
+        while (k0 + 1 < radix &&
+               !(mem_kO(tc, rs, (double)((MODE == 2) ? A.vals[k0] : k0), Q) <= tc.DMB))
+            ++k0;
+        if (MODE == 0 && A.fp)
+            for (unsigned k = k0; k < radix; ++k) {
+                const u64 idx = idx0 + (u64)k * Q1;
+                if (mem_kO(tc, rs, (double)k, Q) <= tc.DMB) { fcnt++; fhash += splitmix64(idx); }
+            }
+        for (unsigned k = k0; k < radix; ++k) {
+            const unsigned ko = (MODE == 2) ? A.vals[k] : k;
+            const double kO = ko;
+            const double memD = mem_kO(tc, rs, kO, Q);
+            if (!(memD <= tc.DMB)) continue;                 // Eq. 4 constraint, exact
+            const u64 idx = idx0 + (u64)ko * Q1;
+            if (MODE == 0 && !P.ykey) {
+                double scale;
+                const double lb = d_lower_bound(tc, rs, kO, scale);
+                const double thr = best_y < y_thr ? best_y : y_thr;
+                if (lb - 1e-12 * scale > thr) {
+                    if (A.fp) continue;                       // keep counting feasible configs
+                    break;
+                }
+            }
+            // P13: the whole run shares t; keep its min (y, idx)
+            if (!P.ykey) nph += nrows;
+            const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, rs, kO, FG);
+            if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
+        }
+    }
+    if (MODE == 0 && has && A.f_off) {
+        // staircase filter: the pilot frontier point with the largest t <= rt has the
+        // smallest y among all pilot points with t <= rt; if it beats the run's best,
+        // drop it (exact: it is a real feasible config of the same group, O10)
+        long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
+        const double rt = rs.t;
+        while (lo < hi) {                       // first position with f_t > rt
+            const long long mid = (lo + hi) >> 1;
+            if (__ldg(A.f_t + mid) <= rt) lo = mid + 1; else hi = mid;
+        }
+        if (lo > A.f_off[grp]) {
+            const long long k = lo - 1;
+            if (beats(__ldg(A.f_t + k), __ldg(A.f_y + k), __ldg(A.f_idx + k), rt, best_y, best_i))
+                has = false;
+        }
+    }
+    RunCand r;
+    r.has = has; r.t = rs.t; r.y = best_y; r.m = best_m; r.idx = best_i;
+    return r;
+}
+
 // One thread per unit = (tuple, kW, kA); it loops over kG (runs) and kO
 // (configs).  Units of one tuple are padded to a multiple of 32 when there are
 // >= 64 of them, so that a warp never straddles two tuples (the phase
@@ -461,69 +565,10 @@ k_eval(DevProblem P, EvalArgs A) {
                         if (A.mem) A.mem[o] = memD / tc.D;
                         if (A.feas) A.feas[o] = memD <= tc.DMB;
                     }
-                } else if (mem_kO(tc, rs, Q, Q) <= tc.DMB) {
-                    // D*mem is non-increasing in kO (O9: P_raw >= min(l,2) P_layer), so the
-                    // feasible configs of a run are a suffix in kO and a run whose kO = Q
-                    // config is over budget has none: its t and d are never needed (R2).
-                    run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
-                    nph += brows;
-                    // Bound-and-skip (ykey = d): a config whose lower bound of d exceeds the
-                    // best d the run already has, or the y of a known feasible point with
-                    // t <= the run's t (pilot staircase / cached candidate, both with a
-                    // smaller-or-unrelated idx, so equal y is not needed), cannot be the run's
-                    // frontier candidate.  The bound is non-decreasing in kO (R4).
-                    double y_thr = CUDART_INF;
-                    if (MODE == 0 && !P.ykey) {
-                        if (cv && ct <= rs.t) y_thr = cy;
-                        if (A.f_off) {
-                            long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
-                            while (lo < hi) {
-                                const long long mid = (lo + hi) >> 1;
-                                if (__ldg(A.f_t + mid) <= rs.t) lo = mid + 1; else hi = mid;
-                            }
-                            if (lo > A.f_off[grp]) {
-                                const double yf = __ldg(A.f_y + lo - 1);
-                                y_thr = yf < y_thr ? yf : y_thr;
-                            }
-                        }
-                    }
-                    for (unsigned k = 0; k < radix; ++k) {
-                        const unsigned ko = (MODE == 2) ? A.vals[k] : k;
-                        const double kO = ko;
-                        const double memD = mem_kO(tc, rs, kO, Q);
-                        if (!(memD <= tc.DMB)) continue;                 // Eq. 4 constraint, exact
-                        const u64 idx = idx0 + (u64)ko * Q1;
-                        if (MODE == 0 && A.fp) { fcnt++; fhash += splitmix64(idx); }
-                        if (MODE == 0 && !P.ykey) {
-                            double scale;
-                            const double lb = d_lower_bound(tc, rs, kO, scale);
-                            const double thr = best_y < y_thr ? best_y : y_thr;
-                            if (lb - 1e-12 * scale > thr) {
-                                if (A.fp) continue;                       // keep counting feasible configs
-                                break;
-                            }
-                        }
-                        // P13: the whole run shares t; keep its min (y, idx)
-                        if (!P.ykey) nph += nrows;
-                        const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, rs, kO, FG);
-                        if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
-                    }
-                }
-                if (MODE == 0 && has && A.f_off) {
-                    // staircase filter: the pilot frontier point with the largest t <= rt has the
-                    // smallest y among all pilot points with t <= rt; if it beats the run's best,
-                    // drop it (exact: it is a real feasible config of the same group, O10)
-                    long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
-                    const double rt = rs.t;
-                    while (lo < hi) {                       // first position with f_t > rt
-                        const long long mid = (lo + hi) >> 1;
-                        if (__ldg(A.f_t + mid) <= rt) lo = mid + 1; else hi = mid;
-                    }
-                    if (lo > A.f_off[grp]) {
-                        const long long k = lo - 1;
-                        if (beats(__ldg(A.f_t + k), __ldg(A.f_y + k), __ldg(A.f_idx + k), rt, best_y, best_i))
-                            has = false;
-                    }
+                } else {
+                    const RunCand rc = frontier_run<UNIT, MODE>(P, A, tc, us, kW, kG, kA, radix, Q, Q1, grp, FG, cv,
+                                                                ct, cy, nrows, brows, nph, fcnt, fhash);
+                    has = rc.has; best_y = rc.y; best_i = rc.idx; best_m = rc.m; rs.t = rc.t;
                 }
                 if (MODE != 1 && has) {
                     const double rt = rs.t, rm = best_m / tc.D;
@@ -571,6 +616,142 @@ k_eval(DevProblem P, EvalArgs A) {
                 }
             }
         }
+    }
+}
+
+// Frontier mode with a warp-level run queue.  Every lane first finds its
+// unit's first run (kG) whose kO = Q config fits the budget; with D*mem
+// non-increasing in kG (mG >= gb_k, true for 2-byte gradients) the feasible
+// runs of a unit are a suffix in kG (R2').  The warp then deals the feasible
+// runs of its 32 units round-robin to its lanes (owner found by binary lifting
+// over the warp prefix sum, unit state fetched with shuffles), so no lane idles
+// on an infeasible run while another works.
+template <bool UNIT, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+k_eval_q(DevProblem P, EvalArgs A) {
+    extern __shared__ double smem[];
+    FGRow* FG = reinterpret_cast<FGRow*>(smem);
+    TupleConst* sT = reinterpret_cast<TupleConst*>(smem + 128);
+    const int tid = threadIdx.x;
+    load_fg(P, FG, tid);
+    const double Q = P.Q;
+    const int Q1 = P.Q1;
+    const unsigned lane = tid & 31;
+    const unsigned radix = (unsigned)Q1;
+    const unsigned upt = A.upt;
+    const u64 n_units = A.n_units;
+    unsigned nph = 0;
+    for (u64 base = (u64)blockIdx.x * NT; base < n_units; base += (u64)gridDim.x * NT) {
+        const u64 last_unit = min(base + NT, n_units) - 1;
+        const u64 tb0 = base / upt, tb1 = last_unit / upt;
+        const int ntl = (int)(tb1 - tb0 + 1);
+        __syncthreads();
+        {
+            const double* src = reinterpret_cast<const double*>(A.tuples + tb0);
+            double* dst = reinterpret_cast<double*>(sT);
+            const int nw = ntl * (int)(sizeof(TupleConst) / 8);
+            for (int i = tid; i < nw; i += NT) dst[i] = __ldg(src + i);
+        }
+        __syncthreads();
+        const u64 u = base + tid;
+        const unsigned tk = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
+        const unsigned jj = (unsigned)(u - (tb0 + tk) * (u64)upt);
+        const bool active = u < n_units && jj < radix * radix;
+        const unsigned kW = jj / radix, kA = jj - kW * radix;
+        UnitState us;
+        unsigned g0 = radix;
+        {
+            const TupleConst& tc = sT[tk];
+            if (active) {
+                unit_forward<UNIT>(tc, (double)kW, (double)kA, FG, us);
+                nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
+                       (unsigned)(tc.last != 0);
+                RunState rm;
+                for (unsigned ig = 0; ig < radix; ++ig) {
+                    run_memory(tc, (double)kW, (double)ig, (double)kA, Q, rm);
+                    if (mem_kO(tc, rm, Q, Q) <= tc.DMB) { g0 = ig; break; }
+                }
+                if (!(tc.mG >= tc.gb_k)) g0 = 0;      // no kG-suffix property: every run is a task
+            }
+        }
+        const unsigned cnt = active ? radix - g0 : 0u;
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += v;
+        }
+        const unsigned excl = incl - cnt;
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        bool cv = false;                        // cached candidate (any group; emitted on group change)
+        double ct = 0.0, cy = 0.0, cm = 0.0;
+        u64 ci = 0;
+        unsigned cgrp = 0;
+        for (unsigned rb = 0; rb < total; rb += 32) {
+            const unsigned r = rb + lane;
+            unsigned own = 0;                   // largest lane whose excl <= r
+#pragma unroll
+            for (int s2 = 16; s2 > 0; s2 >>= 1) {
+                const unsigned cand = own + s2;
+                const unsigned e = __shfl_sync(0xffffffffu, excl, cand & 31);
+                if (cand < 32 && e <= r) own = cand;
+            }
+            const unsigned o_tk = __shfl_sync(0xffffffffu, tk, own);
+            const unsigned o_kW = __shfl_sync(0xffffffffu, kW, own);
+            const unsigned o_kA = __shfl_sync(0xffffffffu, kA, own);
+            const unsigned o_g0 = __shfl_sync(0xffffffffu, g0, own);
+            const unsigned o_ex = __shfl_sync(0xffffffffu, excl, own);
+            UnitState ou;
+            ou.tf = __shfl_sync(0xffffffffu, us.tf, own);
+            ou.FH_L = __shfl_sync(0xffffffffu, us.FH_L, own);
+            ou.FH_E = __shfl_sync(0xffffffffu, us.FH_E, own);
+            ou.FH_H = __shfl_sync(0xffffffffu, us.FH_H, own);
+            ou.FD_L0 = __shfl_sync(0xffffffffu, us.FD_L0, own);
+            ou.FD_L1 = __shfl_sync(0xffffffffu, us.FD_L1, own);
+            ou.FD_E = __shfl_sync(0xffffffffu, us.FD_E, own);
+            ou.FD_H = __shfl_sync(0xffffffffu, us.FD_H, own);
+            bool emit = false;
+            double et = 0.0, ey = 0.0, em = 0.0;
+            u64 ei = 0;
+            unsigned egrp = 0;
+            if (r < total) {
+                const TupleConst& tc = sT[o_tk];
+                const unsigned grp = tc.group;
+                const unsigned kG = o_g0 + (r - o_ex);
+                const unsigned nrows = (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) +
+                                       (unsigned)(tc.first != 0) + (unsigned)(tc.last != 0);
+                const unsigned brows = nrows * (tc.L.N_Bp != tc.L.N_B ? 2u : 1u);
+                const bool same = cv && cgrp == grp;
+                u64 fcnt = 0, fhash = 0;
+                const RunCand rc = frontier_run<UNIT, 0>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
+                                                         ct, cy, nrows, brows, nph, fcnt, fhash);
+                if (A.fp && fcnt) {
+                    atomicAdd(A.fp + 2 * (u64)grp, fcnt);
+                    atomicAdd(A.fp + 2 * (u64)grp + 1, fhash);
+                }
+                if (rc.has) {
+                    const double rm = rc.m / tc.D;
+                    if (!cv) {
+                        cv = true; ct = rc.t; cy = rc.y; cm = rm; ci = rc.idx; cgrp = grp;
+                    } else if (same && beats(ct, cy, ci, rc.t, rc.y, rc.idx)) {
+                        // the new run's best is beaten by the cached point: drop it
+                    } else {
+                        if (!same || !beats(rc.t, rc.y, rc.idx, ct, cy, ci)) {   // incomparable: emit the cached one
+                            emit = true; et = ct; ey = cy; em = cm; ei = ci; egrp = cgrp;
+                        }
+                        ct = rc.t; cy = rc.y; cm = rm; ci = rc.idx; cgrp = grp;
+                    }
+                }
+            }
+            warp_emit(emit, et, ey, em, ei, egrp, A, lane);
+        }
+        warp_emit(cv, ct, cy, cm, ci, cgrp, A, lane);
+    }
+    if (A.phases) {
+        unsigned v = nph;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(A.phases, (u64)v);
     }
 }
 
@@ -678,8 +859,44 @@ static int eval_cfg() {
     return v;
 }
 
+template <bool UNIT, int NT, int MINB>
+static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
+    const size_t smem = eval_smem_bytes(A.upt);
+    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB>, NT, smem);
+    if (per_sm < 1) per_sm = 1;
+    u64 blocks = (A.n_units + NT - 1) / NT;
+    const u64 cap = (u64)sm_count(device) * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) return cudaSuccess;
+    k_eval_q<UNIT, NT, MINB><<<(unsigned)blocks, NT, smem, st>>>(P, A);
+    return cudaGetLastError();
+}
+
+// MIST_EVAL_QUEUE=0 selects the lockstep kG loop instead of the warp run queue.
+static bool eval_queue() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("MIST_EVAL_QUEUE");
+        v = (s && s[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <bool UNIT>
 static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
+    if (eval_queue()) {
+        switch (eval_cfg()) {
+            case 0: return launch_eval_q<UNIT, 256, 2>(st, device, P, A);
+            default: return launch_eval_q<UNIT, 256, 3>(st, device, P, A);
+        }
+    }
     switch (eval_cfg()) {
         case 1: return launch_eval_t<UNIT, 0, 256, 3>(st, device, P, A);
         case 2: return launch_eval_t<UNIT, 0, 128, 4>(st, device, P, A);

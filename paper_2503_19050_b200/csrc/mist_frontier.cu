@@ -155,10 +155,15 @@ __global__ void k_radix_upsweep(const u64* __restrict__ t, const u32* __restrict
     h[threadIdx.x] = 0;
     __syncthreads();
     const long long base = (long long)blockIdx.x * kSortTile;
-    for (int j = 0; j < kSortItems; ++j) {
+    u32 dg[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {            // issue every load of the tile first (MLP)
         const long long i = base + (long long)j * kThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[digit_of(pos < 8 ? t[i] : 0ull, pos < 8 ? 0u : g[i], pos)], 1u);
+        dg[j] = i < n ? digit_of(pos < 8 ? t[i] : 0ull, pos < 8 ? 0u : g[i], pos) : 256u;
     }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j)
+        if (dg[j] < 256u) atomicAdd(&h[dg[j]], 1u);
     __syncthreads();
     block_hist[(long long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
@@ -190,12 +195,16 @@ k_radix_scatter(const u64* __restrict__ t_in, const u32* __restrict__ g_in,
     u32 gv[kSortItems], vv[kSortItems], dg[kSortItems], rk[kSortItems];
     const u32 lt = (1u << lane) - 1;
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
+    for (int j = 0; j < kSortItems; ++j) {            // issue every load of the sub-tile first (MLP)
         const long long i = wbase + j * 32 + lane;
         const bool valid = i < n;
         tv[j] = valid ? t_in[i] : 0ull;
         gv[j] = valid ? g_in[i] : 0u;
         vv[j] = valid ? v_in[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const bool valid = wbase + j * 32 + lane < n;
         dg[j] = valid ? digit_of(tv[j], gv[j], pos) : 0xffffffffu;
         const u32 peers = __match_any_sync(0xffffffffu, dg[j]);
         const u32 before = valid ? s_cnt[w][dg[j]] : 0u;
@@ -316,10 +325,21 @@ struct FsIn {
     const u64* t;      // sorted t bits
     const u32* g;      // sorted group
     const u32* v;      // payload (candidate position)
-    const double* y;   // candidate y (indexed by payload)
-    const u64* idx;    // candidate idx (indexed by payload)
+    const double* y;   // y in sorted order (gathered once, k_gather_sorted)
+    const u64* idx;    // idx in sorted order
     long long n;
 };
+
+// one random-access pass: y and idx into sorted order, so the scans read coalesced
+__global__ void k_gather_sorted(const u32* __restrict__ v, long long n, const double* __restrict__ y,
+                                const u64* __restrict__ idx, double* __restrict__ ys, u64* __restrict__ xs) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const u32 p = v[i];
+        ys[i] = __ldg(y + p);
+        xs[i] = __ldg(idx + p);
+    }
+}
 
 __device__ __forceinline__ FS fs_element(const FsIn& in, long long i) {
     FS s;
@@ -329,7 +349,7 @@ __device__ __forceinline__ FS fs_element(const FsIn& in, long long i) {
     const bool hh = gh || in.t[i - 1] != t;
     const u32 p = in.v[i];
     s.gh = gh; s.hh = hh; s.pre = CUDART_INF;
-    s.cy = in.y[p]; s.cidx = in.idx[p]; s.cpos = p;
+    s.cy = in.y[i]; s.cidx = in.idx[i]; s.cpos = p;
     return s;
 }
 
@@ -485,9 +505,11 @@ cudaError_t frontier_reduce(cudaStream_t st, CandBuf cand, long long n, SortScra
         cur ^= 1;
     }
     // segmented frontier scan over the sorted keys
+    k_gather_sorted<<<grid_for(n, T), T, 0, st>>>(S.val[cur], n, cand.y, cand.idx, S.gy, S.gidx);
+    rs->launches++;
     FsIn in;
     in.t = S.key_t[cur]; in.g = S.key_g[cur]; in.v = S.val[cur];
-    in.y = cand.y; in.idx = cand.idx; in.n = n;
+    in.y = S.gy; in.idx = S.gidx; in.n = n;
     const long long ftiles = (n + kFsTile - 1) / kFsTile;
     FS* tile_agg = reinterpret_cast<FS*>(S.block_hist);   // reuse (ntiles*256 u32 >= ftiles FS)
     u32* flag = S.val[cur ^ 1];

@@ -91,6 +91,8 @@ struct SortScratch {
     unsigned* val[2] = {nullptr, nullptr};
     unsigned* block_hist = nullptr;    // [256][tiles]
     unsigned* digit_hist = nullptr;    // [12][256] global histograms
+    double* gy = nullptr;              // y gathered into sorted order
+    unsigned long long* gidx = nullptr;   // idx gathered into sorted order
     long long cap = 0;
     long long hist_cap = 0;
 };
