@@ -389,16 +389,27 @@ struct RunCand {
     u64 idx;
 };
 
+// The pilot staircase as seen by one CTA: global arrays, or a shared-memory copy
+// of the CTA's groups addressed with the global positions (pointers shifted).
+struct FiltView {
+    const double* t;
+    const double* y;
+    const u64* idx;
+    const int64_t* off;     // null: no filter
+};
+
 template <bool UNIT, int MODE>
 __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalArgs& A, const TupleConst& tc,
                                                 const UnitState& us, unsigned kW, unsigned kG, unsigned kA,
                                                 unsigned radix, double Q, int Q1, unsigned grp, const FGRow* FG,
                                                 bool cv, double ct, double cy, unsigned nrows, unsigned brows,
-                                                unsigned& nph, u64& fcnt, u64& fhash) {
+                                                unsigned& nph, u64& fcnt, u64& fhash, const FiltView& fv) {
     const double dkW = kW, dkG = kG, dkA = kA;
     RunState rs;
     run_memory(tc, dkW, dkG, dkA, Q, rs);
     rs.t = 0.0;
+    const long long f_lo = (MODE == 0 && fv.off) ? fv.off[grp] : 0;
+    long long f_at = f_lo - 1;              // staircase point used by the filter (none if < f_lo)
     const u64 idx0 = tc.idx_base + ((u64)(kW * Q1 + kG) * Q1) * Q1 + kA;
     bool has = false;
     double best_y = CUDART_INF, best_m = 0.0;
@@ -414,19 +425,21 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
         // t <= the run's t (pilot staircase / cached candidate, both with a
         // smaller-or-unrelated idx, so equal y is not needed), cannot be the run's
         // frontier candidate.  The bound is non-decreasing in kO (R4).
+        // the staircase point with the largest t <= the run's t (one binary search, reused below)
+        if (MODE == 0 && fv.off) {
+            long long lo = f_lo, hi = fv.off[grp + 1];
+            while (lo < hi) {                       // first position with f_t > t
+                const long long mid = (lo + hi) >> 1;
+                if (fv.t[mid] <= rs.t) lo = mid + 1; else hi = mid;
+            }
+            f_at = lo - 1;
+        }
         double y_thr = CUDART_INF;
         if (MODE == 0 && !P.ykey) {
             if (cv && ct <= rs.t) y_thr = cy;
-            if (A.f_off) {
-                long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
-                while (lo < hi) {
-                    const long long mid = (lo + hi) >> 1;
-                    if (__ldg(A.f_t + mid) <= rs.t) lo = mid + 1; else hi = mid;
-                }
-                if (lo > A.f_off[grp]) {
-                    const double yf = __ldg(A.f_y + lo - 1);
-                    y_thr = yf < y_thr ? yf : y_thr;
-                }
+            if (f_at >= f_lo) {
+                const double yf = fv.y[f_at];
+                y_thr = yf < y_thr ? yf : y_thr;
             }
         }
         // First feasible config of the run: the feasible configs are a suffix in kO
@@ -462,21 +475,11 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
         }
     }
-    if (MODE == 0 && has && A.f_off) {
+    if (MODE == 0 && has && f_at >= f_lo) {
         // staircase filter: the pilot frontier point with the largest t <= rt has the
         // smallest y among all pilot points with t <= rt; if it beats the run's best,
         // drop it (exact: it is a real feasible config of the same group, O10)
-        long long lo = A.f_off[grp], hi = A.f_off[grp + 1];
-        const double rt = rs.t;
-        while (lo < hi) {                       // first position with f_t > rt
-            const long long mid = (lo + hi) >> 1;
-            if (__ldg(A.f_t + mid) <= rt) lo = mid + 1; else hi = mid;
-        }
-        if (lo > A.f_off[grp]) {
-            const long long k = lo - 1;
-            if (beats(__ldg(A.f_t + k), __ldg(A.f_y + k), __ldg(A.f_idx + k), rt, best_y, best_i))
-                has = false;
-        }
+        if (beats(fv.t[f_at], fv.y[f_at], fv.idx[f_at], rs.t, best_y, best_i)) has = false;
     }
     RunCand r;
     r.has = has; r.t = rs.t; r.y = best_y; r.m = best_m; r.idx = best_i;
@@ -566,8 +569,10 @@ k_eval(DevProblem P, EvalArgs A) {
                         if (A.feas) A.feas[o] = memD <= tc.DMB;
                     }
                 } else {
+                    FiltView fv;
+                    fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
                     const RunCand rc = frontier_run<UNIT, MODE>(P, A, tc, us, kW, kG, kA, radix, Q, Q1, grp, FG, cv,
-                                                                ct, cy, nrows, brows, nph, fcnt, fhash);
+                                                                ct, cy, nrows, brows, nph, fcnt, fhash, fv);
                     has = rc.has; best_y = rc.y; best_i = rc.idx; best_m = rc.m; rs.t = rc.t;
                 }
                 if (MODE != 1 && has) {
@@ -653,6 +658,8 @@ k_eval_q(DevProblem P, EvalArgs A) {
             for (int i = tid; i < nw; i += NT) dst[i] = __ldg(src + i);
         }
         __syncthreads();
+        FiltView fv;
+        fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
         const u64 u = base + tid;
         const unsigned tk = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
         const unsigned jj = (unsigned)(u - (tb0 + tk) * (u64)upt);
@@ -724,7 +731,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                 const bool same = cv && cgrp == grp;
                 u64 fcnt = 0, fhash = 0;
                 const RunCand rc = frontier_run<UNIT, 0>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
-                                                         ct, cy, nrows, brows, nph, fcnt, fhash);
+                                                         ct, cy, nrows, brows, nph, fcnt, fhash, fv);
                 if (A.fp && fcnt) {
                     atomicAdd(A.fp + 2 * (u64)grp, fcnt);
                     atomicAdd(A.fp + 2 * (u64)grp + 1, fhash);
@@ -861,6 +868,7 @@ static int eval_cfg() {
 
 template <bool UNIT, int NT, int MINB>
 static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
+    static_assert(NT == kEvalThreads, "eval_smem_bytes sizes the tuple region for kEvalThreads");
     const size_t smem = eval_smem_bytes(A.upt);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
