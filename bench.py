@@ -12,7 +12,7 @@ NCCL merge when N > 1) ending in the exact per-group Pareto frontiers.
 Default workload: BASELINE.json configs[1] = cfg2, GPT-3 2.7B on a modelled
 8-GPU mesh, B=64, s=2048, offload ratios in 0.1 steps (Q=10), ZeRO 0-3:
 7,342,344,372 configurations in 4,569 groups.  The space is sharded across
-ranks by tuple range (strong scaling: total work fixed).
+ranks by block-cyclic tuple ranges (strong scaling: total work fixed).
 
 --impl reference times the CPU oracle (the reference arm of this tier) on a
 bounded sample of the same workload, on the host cores.

@@ -166,14 +166,20 @@ mist_status_t mist_ctx_set_timing(mist_ctx_t* ctx, int enabled);
  * frontiers over NVLink (ncclAllGather) and returns the merged global
  * frontier on every rank. */
 mist_status_t mist_nccl_unique_id(uint8_t id[MIST_NCCL_ID_BYTES]);
-/* Host-only: the equal contiguous share [t_begin, t_end) of the global tuple
- * range [0, n_tuples) that `rank` of `world` evaluates when
- * mist_pareto_frontier is called with t_end == 0 and a communicator
- * (t_begin = floor(n_tuples*rank/world)).  Every tuple holds (Q+1)^4 configs,
- * so shares are equal in configs.  INVALID_ARG if rank/world
- * are out of range. */
-mist_status_t mist_shard_range(uint64_t n_tuples, int rank, int world, uint64_t* t_begin,
-                               uint64_t* t_end);
+/* Host-only: the tuple ranges that `rank` of `world` evaluates when
+ * mist_pareto_frontier is called with t_end == 0 and a communicator.
+ * Block-cyclic (SURVEY 8(e) "weight ranges if the measured imbalance exceeds a
+ * few percent"): [0, n_tuples) is cut into nb = world*K blocks at
+ * floor(n_tuples*i/nb), K = clamp(n_tuples/(world*2048), 1, 64), and rank r
+ * owns blocks i = r (mod world); adjacent owned blocks are coalesced.  Every
+ * tuple holds (Q+1)^4 configs, so shares are equal in configs to within one
+ * tuple per block, and the per-tuple cost, which varies by orders of
+ * magnitude along the group order, is sampled evenly by every rank.
+ * Two-call pattern: begins/ends == NULL (or cap too small) => *n_ranges is
+ * set (MIST_ERR_BUFFER_TOO_SMALL when the buffers are too small).
+ * INVALID_ARG if rank/world are out of range. */
+mist_status_t mist_shard_ranges(uint64_t n_tuples, int rank, int world, uint64_t* begins,
+                                uint64_t* ends, int64_t cap, int64_t* n_ranges);
 mist_status_t mist_ctx_init_comm(mist_ctx_t* ctx, const uint8_t id[MIST_NCCL_ID_BYTES],
                                  int rank, int world);
 
@@ -214,7 +220,7 @@ mist_status_t mist_eval_stage_costs_at(mist_ctx_t* ctx, const mist_model_t* mode
 
 /* ---- a2-a11: the sweep ---------------------------------------------------
  * Evaluates the global tuple range [t_begin, t_end) (t_end == 0 => all
- * tuples; with a comm and t_end == 0, this rank's equal share), keeps
+ * tuples; with a comm and t_end == 0, this rank's mist_shard_ranges share), keeps
  * feasible configs, and returns the exact per-group frontier over
  * (x, y) = (t, d) or (t, mem) (O10): point p beats q iff x_p <= x_q,
  * y_p <= y_q and (x_p < x_q or y_p < y_q or idx_p < idx_q); the frontier is

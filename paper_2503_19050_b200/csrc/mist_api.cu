@@ -86,32 +86,44 @@ static mist_status_t cuda_fail(mist_ctx_t* ctx, cudaError_t e, const char* where
 
 static int ev_begin(mist_ctx_t* ctx, int cat) {
     if (!ctx->timing) return -1;
-    const int base = (int)ctx->ev_used.size() * 2;
-    while ((int)ctx->ev_pool.size() < base + 2) {
-        cudaEvent_t e;
-        if (cudaEventCreate(&e) != cudaSuccess) return -1;
-        ctx->ev_pool.push_back(e);
+    int base;
+    if (!ctx->ev_free.empty()) {
+        base = ctx->ev_free.back();
+        ctx->ev_free.pop_back();
+    } else {
+        base = (int)ctx->ev_pool.size();
+        for (int i = 0; i < 2; ++i) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return -1;
+            ctx->ev_pool.push_back(e);
+        }
     }
     cudaEventRecord(ctx->ev_pool[base], ctx->stream);
-    ctx->ev_used.push_back({cat, base});
+    ctx->ev_used.push_back({cat, base, false});
     return base;
 }
 
 static void ev_end(mist_ctx_t* ctx, int h) {
     if (h < 0) return;
     cudaEventRecord(ctx->ev_pool[h + 1], ctx->stream);
+    for (auto it = ctx->ev_used.rbegin(); it != ctx->ev_used.rend(); ++it)
+        if (it->base == h) { it->done = true; break; }
 }
 
+// Reads every closed interval; open ones (e.g. the whole-call total) keep their events.
 static void ev_flush(mist_ctx_t* ctx) {
     if (ctx->ev_used.empty()) return;
     cudaStreamSynchronize(ctx->stream);
+    std::vector<mist_ctx::EvUse> open;
     for (auto& u : ctx->ev_used) {
+        if (!u.done) { open.push_back(u); continue; }
+        ctx->ev_free.push_back(u.base);
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, ctx->ev_pool[u.second], ctx->ev_pool[u.second + 1]) != cudaSuccess) {
+        if (cudaEventElapsedTime(&ms, ctx->ev_pool[u.base], ctx->ev_pool[u.base + 1]) != cudaSuccess) {
             cudaGetLastError();
             continue;
         }
-        switch (u.first) {
+        switch (u.cat) {
             case CAT_EVAL: ctx->stats.eval_ms += ms; break;
             case CAT_PRE: ctx->stats.precompute_ms += ms; break;
             case CAT_RED: ctx->stats.reduce_ms += ms; break;
@@ -120,7 +132,7 @@ static void ev_flush(mist_ctx_t* ctx) {
             case CAT_PILOT: ctx->stats.pilot_ms += ms; break;
         }
     }
-    ctx->ev_used.clear();
+    ctx->ev_used.swap(open);
 }
 
 static void maybe_flush(mist_ctx_t* ctx) {
@@ -212,6 +224,7 @@ static mist_status_t prepare(mist_ctx_t* ctx, const mist_model_t* model, int64_t
 
 static void reset_stats(mist_ctx_t* ctx) {
     std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+    for (auto& u : ctx->ev_used) ctx->ev_free.push_back(u.base);
     ctx->ev_used.clear();
 }
 
@@ -560,8 +573,8 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     A.fp = mode == 0 ? S.d_fp : nullptr;
     A.phases = mode == 0 ? S.d_phases : nullptr;
     A.nv = nv;
-    for (unsigned i = 0; i < nv && i < 4; ++i) A.vals[i] = vals[i];
-    if (mode == 0 && S.filter) {
+    for (unsigned i = 0; i < nv && i < 16; ++i) A.vals[i] = vals[i];
+    if ((mode == 0 || mode == 2) && S.filter) {
         A.f_t = ctx->cand.t;
         A.f_y = ctx->cand.y;
         A.f_idx = ctx->cand.idx;
@@ -598,9 +611,11 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     return MIST_OK;
 }
 
-static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, bool want_fp,
-                           long long* n_front) {
-    const u64 total_runs = (te - tb) * pp.R3;
+static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vector<std::pair<u64, u64>>& ranges,
+                           bool want_fp, long long* n_front) {
+    u64 n_tuples = 0;
+    for (auto& r : ranges) n_tuples += r.second - r.first;
+    const u64 total_runs = n_tuples * pp.R3;
     SweepCtx S;
     S.pp = &pp;
     S.want_fp = want_fp;
@@ -610,7 +625,20 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, 
     if (st != MIST_OK) return st;
     S.C = ctx->cand.cap;
     // tuple table: whole range, at most 4M tuples (2.2 GB) per chunk
-    const u64 chunk_T = std::min<u64>(te - tb, 1ull << 22);
+    // chunks of <= 4M tuples; one chunk packs the rank's ranges back to back (the
+    // eval kernels address tuples through the table, TupleConst carries idx_base)
+    const u64 chunk_T = std::min<u64>(n_tuples, 1ull << 22);
+    std::vector<std::vector<std::pair<u64, u64>>> chunks(1);
+    u64 fill = 0;
+    for (const auto& rg : ranges) {
+        for (u64 a = rg.first; a < rg.second;) {
+            if (fill == chunk_T) { chunks.emplace_back(); fill = 0; }
+            const u64 b = std::min<u64>(rg.second, a + (chunk_T - fill));
+            chunks.back().push_back({a, b});
+            fill += b - a;
+            a = b;
+        }
+    }
     CK(ensure(ctx->tuples, sizeof(TupleConst) * chunk_T), "alloc tuples");
     CK(ensure(ctx->counters, 64), "alloc counters");
     CK(ensure(ctx->foff, sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc filter offsets");
@@ -626,30 +654,50 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, 
         S.d_fp_save = S.d_fp + 2 * (size_t)pp.ng;
         CK(cudaMemsetAsync(S.d_fp, 0, sizeof(u64) * 2 * (size_t)pp.ng, ctx->stream), "zero fp");
     }
-    // pilot sub-grid {0, Q/2, Q} (Q >= 8) or {0, Q} on every ratio axis
+    // pilot levels: sub-grids of nv evenly spaced values on every ratio axis, each
+    // filtered by the staircase of the levels before it; a level costs at most
+    // nv^4/(Q+1)^4 of the sweep.  MIST_PILOT_LEVELS="a,b,..." overrides.
     const unsigned Q = (unsigned)pp.P.Q;
-    unsigned vals[4] = {0, Q, 0, 0}, nv = 2;
-    if (Q >= 8) { vals[1] = Q / 2; vals[2] = Q; nv = 3; }
+    std::vector<unsigned> levels;
+    if (const char* e = getenv("MIST_PILOT_LEVELS")) {
+        for (const char* p = e; *p;) {
+            const int v = atoi(p);
+            if (v >= 2) levels.push_back((unsigned)std::min(16, v));
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+        }
+    } else {
+        levels.push_back(Q < 8 ? 2 : Q < 16 ? 3 : Q < 40 ? 5 : 7);
+    }
+    for (auto& nv : levels) nv = std::min(nv, Q + 1);
     const char* env = getenv("MIST_PILOT");
     const bool pilot = !(env && env[0] == '0') && Q >= 2 && total_runs >= (1ull << 22);
-    for (u64 T0 = tb; T0 < te; T0 += chunk_T) {
-        const u64 nT = std::min<u64>(chunk_T, te - T0);
+    for (const auto& ch : chunks) {
+        u64 nT = 0;
         int h = ev_begin(ctx, CAT_PRE);
-        CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, T0, nT,
-                             (TupleConst*)ctx->tuples.p), "precompute");
+        for (const auto& seg : ch) {
+            CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, seg.first,
+                                 seg.second - seg.first, (TupleConst*)ctx->tuples.p + nT), "precompute");
+            nT += seg.second - seg.first;
+            ctx->stats.kernel_launches += 1;
+        }
         ev_end(ctx, h);
-        ctx->stats.kernel_launches += 1;
         const TupleConst* tup = (const TupleConst*)ctx->tuples.p;
         if (pilot) {
-            // a pilot sweep of the sub-grid seeds an exact staircase filter (its points are
+            // pilot sweeps of sub-grids seed an exact staircase filter (their points are
             // real feasible configs of the same groups, so anything they beat is beaten)
-            st = eval_opt(ctx, S, 2, tup, 0, nT, nv, vals);
-            if (st != MIST_OK) return st;
-            st = reduce_buffer(ctx, S);
-            if (st != MIST_OK) return st;
-            ctx->stats.pilot_configs += nT * (u64)nv * nv * nv * nv;
+            for (unsigned nv : levels) {
+                unsigned vals[16] = {0};
+                for (unsigned i = 0; i < nv; ++i)   // round(i*Q/(nv-1))
+                    vals[i] = (unsigned)((2ull * i * Q + (nv - 1)) / (2ull * (nv - 1)));
+                st = eval_opt(ctx, S, 2, tup, 0, nT, nv, vals);
+                if (st != MIST_OK) return st;
+                st = reduce_buffer(ctx, S);
+                if (st != MIST_OK) return st;
+                ctx->stats.pilot_configs += nT * (u64)nv * nv * nv * nv;
+            }
         }
-        st = eval_opt(ctx, S, 0, tup, 0, nT, 0, vals);
+        st = eval_opt(ctx, S, 0, tup, 0, nT, 0, nullptr);
         if (st != MIST_OK) return st;
         ctx->stats.chunks++;
         maybe_flush(ctx);
@@ -664,7 +712,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, u64 tb, u64 te, 
     long long nf = 0;
     st = reduce_now(ctx, S.count, &nf);
     if (st != MIST_OK) return st;
-    ctx->stats.configs_evaluated += (te - tb) * pp.R;
+    ctx->stats.configs_evaluated += n_tuples * pp.R;
     ctx->stats.frontier_points = (uint64_t)nf;
     *n_front = nf;
     return MIST_OK;
@@ -757,21 +805,22 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         ctx->stats.h2d_bytes = sizeof(DevGroup) * (uint64_t)pp.ng + sizeof(double) * 6 * (uint64_t)pp.P.n_b * pp.P.n_tp;
         int htot = ev_begin(ctx, CAT_TOTAL);   // inputs are resident in HBM from here on
         u64 tb = t_begin, te = t_end;
+        std::vector<std::pair<u64, u64>> ranges;
         if (te == 0) {
             if (ctx->nccl && ctx->world > 1) {
-                uint64_t a = 0, b = 0;
-                mist_shard_range(pp.total_tuples, ctx->rank, ctx->world, &a, &b);
-                tb = a;
-                te = b;
+                for (auto& r : mist_shard_blocks(pp.total_tuples, ctx->rank, ctx->world)) ranges.push_back(r);
             } else {
-                tb = 0;
-                te = pp.total_tuples;
+                ranges.push_back({0, pp.total_tuples});
             }
+        } else {
+            if (tb > te || te > pp.total_tuples) return fail(ctx, MIST_ERR_INVALID_ARG, "tuple range out of bounds");
+            ranges.push_back({tb, te});
         }
-        if (tb > te || te > pp.total_tuples) return fail(ctx, MIST_ERR_INVALID_ARG, "tuple range out of bounds");
+        u64 mine = 0;
+        for (auto& r : ranges) mine += r.second - r.first;
         long long nf = 0;
-        if (te > tb) {
-            st = sweep(ctx, pp, tb, te, want_fp, &nf);
+        if (mine > 0) {
+            st = sweep(ctx, pp, ranges, want_fp, &nf);
             if (st != MIST_OK) return st;
         } else {
             CK(ensure(ctx->fp, sizeof(u64) * 2 * (size_t)pp.ng), "alloc fp");

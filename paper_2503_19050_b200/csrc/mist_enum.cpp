@@ -234,13 +234,39 @@ extern "C" mist_status_t mist_enumerate_space(const mist_model_t* model, int64_t
     return MIST_OK;
 }
 
-extern "C" mist_status_t mist_shard_range(uint64_t n_tuples, int rank, int world, uint64_t* t_begin,
-                                          uint64_t* t_end) {
-    if (!t_begin || !t_end || world < 1 || rank < 0 || rank >= world) return MIST_ERR_INVALID_ARG;
-    // floor(n*r/w) without overflow: n < 2^64, w <= 2^31
-    const unsigned __int128 n = n_tuples;
-    *t_begin = (uint64_t)(n * (unsigned)rank / (unsigned)world);
-    *t_end = (uint64_t)(n * (unsigned)(rank + 1) / (unsigned)world);
+namespace {
+// the ranges of mist_shard_ranges (block-cyclic, coalesced)
+std::vector<std::pair<uint64_t, uint64_t>> shard_blocks(uint64_t n, int rank, int world) {
+    const uint64_t W = (uint64_t)world;
+    uint64_t K = n / (W * 2048);
+    K = std::max<uint64_t>(1, std::min<uint64_t>(64, K));
+    const uint64_t nb = W * K;
+    std::vector<std::pair<uint64_t, uint64_t>> out;
+    for (uint64_t i = (uint64_t)rank; i < nb; i += W) {
+        const uint64_t a = (uint64_t)((unsigned __int128)n * i / nb);
+        const uint64_t b = (uint64_t)((unsigned __int128)n * (i + 1) / nb);
+        if (b <= a) continue;
+        if (!out.empty() && out.back().second == a) out.back().second = b;
+        else out.push_back({a, b});
+    }
+    return out;
+}
+}  // namespace
+
+std::vector<std::pair<uint64_t, uint64_t>> mist_shard_blocks(uint64_t n_tuples, int rank, int world) {
+    return shard_blocks(n_tuples, rank, world);
+}
+
+extern "C" mist_status_t mist_shard_ranges(uint64_t n_tuples, int rank, int world, uint64_t* begins,
+                                           uint64_t* ends, int64_t cap, int64_t* n_ranges) {
+    if (!n_ranges || world < 1 || rank < 0 || rank >= world) return MIST_ERR_INVALID_ARG;
+    const auto r = shard_blocks(n_tuples, rank, world);
+    *n_ranges = (int64_t)r.size();
+    if (!begins || !ends || cap < (int64_t)r.size()) return (begins || ends) ? MIST_ERR_BUFFER_TOO_SMALL : MIST_OK;
+    for (size_t i = 0; i < r.size(); ++i) {
+        begins[i] = r[i].first;
+        ends[i] = r[i].second;
+    }
     return MIST_OK;
 }
 

@@ -404,11 +404,13 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
                                                 unsigned radix, double Q, int Q1, unsigned grp, const FGRow* FG,
                                                 bool cv, double ct, double cy, unsigned nrows, unsigned brows,
                                                 unsigned& nph, u64& fcnt, u64& fhash, const FiltView& fv) {
+    // the staircase filter runs in the frontier sweep and in the pilot (both exact, O10)
+    constexpr bool FILT = MODE == 0 || MODE == 2;
     const double dkW = kW, dkG = kG, dkA = kA;
     RunState rs;
     run_memory(tc, dkW, dkG, dkA, Q, rs);
     rs.t = 0.0;
-    const long long f_lo = (MODE == 0 && fv.off) ? fv.off[grp] : 0;
+    const long long f_lo = (FILT && fv.off) ? fv.off[grp] : 0;
     long long f_at = f_lo - 1;              // staircase point used by the filter (none if < f_lo)
     const u64 idx0 = tc.idx_base + ((u64)(kW * Q1 + kG) * Q1) * Q1 + kA;
     bool has = false;
@@ -426,7 +428,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
         // smaller-or-unrelated idx, so equal y is not needed), cannot be the run's
         // frontier candidate.  The bound is non-decreasing in kO (R4).
         // the staircase point with the largest t <= the run's t (one binary search, reused below)
-        if (MODE == 0 && fv.off) {
+        if (FILT && fv.off) {
             long long lo = f_lo, hi = fv.off[grp + 1];
             while (lo < hi) {                       // first position with f_t > t
                 const long long mid = (lo + hi) >> 1;
@@ -435,7 +437,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             f_at = lo - 1;
         }
         double y_thr = CUDART_INF;
-        if (MODE == 0 && !P.ykey) {
+        if (FILT && !P.ykey) {
             if (cv && ct <= rs.t) y_thr = cy;
             if (f_at >= f_lo) {
                 const double yf = fv.y[f_at];
@@ -460,7 +462,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             const double memD = mem_kO(tc, rs, kO, Q);
             if (!(memD <= tc.DMB)) continue;                 // Eq. 4 constraint, exact
             const u64 idx = idx0 + (u64)ko * Q1;
-            if (MODE == 0 && !P.ykey) {
+            if (FILT && !P.ykey) {
                 double scale;
                 const double lb = d_lower_bound(tc, rs, kO, scale);
                 const double thr = best_y < y_thr ? best_y : y_thr;
@@ -475,7 +477,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
         }
     }
-    if (MODE == 0 && has && f_at >= f_lo) {
+    if (FILT && has && f_at >= f_lo) {
         // staircase filter: the pilot frontier point with the largest t <= rt has the
         // smallest y among all pilot points with t <= rt; if it beats the run's best,
         // drop it (exact: it is a real feasible config of the same group, O10)

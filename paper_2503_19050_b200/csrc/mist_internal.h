@@ -112,7 +112,7 @@ struct EvalArgs {
     uint8_t* feas;
     // MODE 2 (pilot): sub-grid of ratio values vals[0..nv) on every axis; R3 = nv^3
     unsigned nv;
-    unsigned vals[4];
+    unsigned vals[16];
     // staircase filter (MODE 0): a per-group frontier of real feasible configs
     // (sorted by t, y strictly decreasing); a candidate beaten by one is dropped
     const double* f_t;
@@ -127,6 +127,9 @@ struct ReduceStats {
 };
 
 }  // namespace mist
+
+// mist_shard_ranges as a vector (mist_enum.cpp)
+std::vector<std::pair<uint64_t, uint64_t>> mist_shard_blocks(uint64_t n_tuples, int rank, int world);
 
 namespace mist {
 struct DevBuf {
@@ -154,6 +157,8 @@ struct mist_ctx {
     uint64_t cache_key = 0;
     int cache_valid = 0;
     // timing events (pairs)
+    struct EvUse { int cat, base; bool done; };
     std::vector<cudaEvent_t> ev_pool;
-    std::vector<std::pair<int, int>> ev_used;   // (category, pool index of start)
+    std::vector<EvUse> ev_used;   // open and closed intervals (pool index of start; end = base + 1)
+    std::vector<int> ev_free;     // pool pairs whose interval has been read
 };

@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-from typing import Optional, Tuple
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -29,7 +29,7 @@ Y_DELTA, Y_MEM = 0, 1
 
 EXPORTED = ("mist_ctx_create", "mist_ctx_destroy", "mist_status_string", "mist_ctx_last_error",
             "mist_ctx_stats", "mist_ctx_set_timing", "mist_nccl_unique_id", "mist_ctx_init_comm",
-            "mist_shard_range",
+            "mist_shard_ranges",
             "mist_enumerate_space", "mist_eval_stage_costs", "mist_eval_stage_costs_at",
             "mist_pareto_frontier", "mist_frontier_points", "mist_sample_frontier")
 
@@ -109,7 +109,7 @@ def lib():
         L.mist_ctx_set_timing.argtypes = [V, C.c_int]
         L.mist_nccl_unique_id.argtypes = [V]
         L.mist_ctx_init_comm.argtypes = [V, V, C.c_int, C.c_int]
-        L.mist_shard_range.argtypes = [C.c_uint64, C.c_int, C.c_int, P(C.c_uint64), P(C.c_uint64)]
+        L.mist_shard_ranges.argtypes = [C.c_uint64, C.c_int, C.c_int, V, V, C.c_int64, P(C.c_int64)]
         L.mist_enumerate_space.argtypes = [P(mist_model_t), C.c_int64, P(mist_mesh_t), P(mist_space_t),
                                            P(mist_coeffs_t), P(mist_group_t), C.c_int64, P(C.c_int64),
                                            P(C.c_uint64)]
@@ -257,13 +257,18 @@ def mist_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def mist_shard_range(n_tuples: int, rank: int, world: int) -> Tuple[int, int]:
-    """This rank's equal contiguous share of the tuple range (host-only)."""
-    a, b = C.c_uint64(0), C.c_uint64(0)
-    st = lib().mist_shard_range(n_tuples, rank, world, C.byref(a), C.byref(b))
+def mist_shard_ranges(n_tuples: int, rank: int, world: int) -> List[Tuple[int, int]]:
+    """This rank's block-cyclic share of the tuple range, as [begin, end) pairs (host-only)."""
+    n = C.c_int64(0)
+    st = lib().mist_shard_ranges(n_tuples, rank, world, None, None, 0, C.byref(n))
     if st != 0:
-        raise MistError(st, "mist_shard_range")
-    return a.value, b.value
+        raise MistError(st, "mist_shard_ranges")
+    b = (C.c_uint64 * max(1, n.value))()
+    e = (C.c_uint64 * max(1, n.value))()
+    st = lib().mist_shard_ranges(n_tuples, rank, world, b, e, n.value, C.byref(n))
+    if st != 0:
+        raise MistError(st, "mist_shard_ranges")
+    return [(b[i], e[i]) for i in range(n.value)]
 
 
 def mist_eval_stage_costs(ctx: Context, spec: Spec, begin: int, end: int, t=None, d=None, mem=None,

@@ -48,7 +48,9 @@ def main():
     wall = time.perf_counter() - t0
     st = ctx.stats()
     w = torch.tensor([wall, st["total_ms"], st["eval_ms"]], dtype=torch.float64, device=dev)
+    per_rank = [w.clone() for _ in range(world)]
     if world > 1:
+        dist.all_gather(per_rank, w)
         dist.all_reduce(w, op=dist.ReduceOp.MAX)
     if rank == 0:
         out = {"workload": args.workload, "n_gpus": world, "configs": spec.n_configs, "groups": spec.n_groups,
@@ -57,7 +59,9 @@ def main():
                "frontier_points": int(len(pts)), "nonempty_groups": int((np.diff(offs) > 0).sum()),
                "pilot_ms": st["pilot_ms"], "reduce_ms": st["reduce_ms"], "merge_ms": st["merge_ms"],
                "phases_per_config": st["phases_evaluated"] / max(1, st["configs_evaluated"]),
-               "rollbacks": st["rollbacks"]}
+               "rollbacks": st["rollbacks"],
+               "eval_s_per_rank": [round(float(x[2]) / 1e3, 3) for x in per_rank],
+               "device_s_per_rank": [round(float(x[1]) / 1e3, 3) for x in per_rank]}
         if args.fingerprints:
             out["feasible_configs"] = int(fc.sum())
         print(json.dumps(out), flush=True)
