@@ -45,34 +45,41 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    """variant "counters": instrumented copy libmist_counters.so (-DMIST_COUNTERS,
+    event counters printed by the sweep); the product library is untouched."""
+    lib_path, build_dir, defs = LIB, BUILD, []
+    if variant == "counters":
+        lib_path, build_dir, defs = os.path.join(PKG, "libmist_counters.so"), BUILD + "_counters", ["-DMIST_COUNTERS"]
+        force = True
     if not force and not _stale():
         return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(build_dir, exist_ok=True)
     nccl_inc, nccl_lib = _nccl_dirs()
     objs = []
     for src in _sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         if src.endswith(".cu"):
-            cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            cmd = ["nvcc", *ARCH, *defs, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc,
                    "-c", src, "-o", obj]
         else:
-            cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", CSRC,
+            cmd = ["g++", *defs, "-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", CSRC,
                    "-I", "/usr/local/cuda/include", "-I", nccl_inc, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = ["nvcc", *ARCH, "-shared", "-o", tmp, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + nccl_lib, "-cudart", "static"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True,
+          variant="counters" if "--counters" in sys.argv else "")

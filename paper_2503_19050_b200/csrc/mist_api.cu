@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -644,7 +645,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     CK(ensure(ctx->foff, sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc filter offsets");
     S.d_count = (u64*)ctx->counters.p;
     S.d_phases = S.d_count + 1;
-    CK(cudaMemsetAsync(S.d_phases, 0, sizeof(u64), ctx->stream), "zero phase counter");
+    CK(cudaMemsetAsync(S.d_phases, 0, 5 * sizeof(u64), ctx->stream), "zero phase counters");
     S.d_foff = (int64_t*)ctx->foff.p;
     st = write_count(ctx, S, 0);
     if (st != MIST_OK) return st;
@@ -704,10 +705,15 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     }
     ctx->stats.candidates += (uint64_t)S.count;   // before the final reduction
     {
-        u64 ph = 0;
-        CK(cudaMemcpyAsync(&ph, S.d_phases, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream), "read phases");
+        u64 ph[5] = {0, 0, 0, 0, 0};
+        CK(cudaMemcpyAsync(ph, S.d_phases, sizeof(ph), cudaMemcpyDeviceToHost, ctx->stream), "read phases");
         CK(cudaStreamSynchronize(ctx->stream), "sync phases");
-        ctx->stats.phases_evaluated += ph;
+        ctx->stats.phases_evaluated += ph[0];
+#ifdef MIST_COUNTERS
+        fprintf(stderr, "MIST_COUNTERS runs_backward=%llu runs_cut_at_k0=%llu d_evals=%llu k0_steps=%llu configs=%llu\n",
+                (unsigned long long)ph[1], (unsigned long long)ph[2], (unsigned long long)ph[3],
+                (unsigned long long)ph[4], (unsigned long long)(n_tuples * pp.R));
+#endif
     }
     long long nf = 0;
     st = reduce_now(ctx, S.count, &nf);

@@ -221,6 +221,26 @@ __device__ __forceinline__ double mem_kO(const TupleConst& tc, const RunState& r
     return dmax(fwd, bwd);
 }
 
+// Smallest feasible kO of a run whose kO = Q config is feasible (R2).  D*Mem_fwd
+// and D*Mem_bwd are affine in kO with slopes -(mO - ob_k) <= 0 and -mO <= 0, so
+// the boundary is max over the two of ceil((D*Mem_X(0) - D*MB) / slope); a
+// float reciprocal gives an under-estimate (error << 1 step) and the exact
+// integer memory test walks it up to the boundary (feasibility is monotone in kO).
+__device__ __forceinline__ unsigned first_feasible_kO(const TupleConst& tc, const RunState& rs, double Q) {
+    if (mem_kO(tc, rs, 0.0, Q) <= tc.DMB) return 0u;
+    const double rb = rs.Kb + tc.mO * Q - tc.DMB;          // bwd(k) <= DMB  <=>  mO k >= rb
+    const double sf = tc.mO - tc.ob_k;
+    const double rf = rs.Kf + tc.mO * Q - tc.DMB;          // fwd(k) <= DMB  <=>  sf k >= rf
+    double g = 0.0;
+    if (rb > 0.0) g = tc.mO > 0.0 ? rb * (double)__frcp_rn((float)tc.mO) : Q;
+    if (rf > 0.0) g = dmax(g, sf > 0.0 ? rf * (double)__frcp_rn((float)sf) : Q);
+    g = g * (1.0 - 1e-5) - 1e-5;                           // under-estimate (float reciprocal: 2^-23 relative)
+    int k = g > 1.0 ? (int)ceil(g < Q ? g : Q) : 1;
+    const int iQ = (int)Q;
+    while (k < iQ && !(mem_kO(tc, rs, (double)k, Q) <= tc.DMB)) ++k;
+    return (unsigned)k;
+}
+
 // F phases of the unit
 template <bool UNIT>
 __device__ __forceinline__ void unit_forward(const TupleConst& tc, double kW, double kA, const FGRow* FG,
@@ -304,28 +324,63 @@ __device__ __forceinline__ double d_kO(const TupleConst& tc, const RunState& rs,
     return ds > 0.0 ? ds : 0.0;                             // L25: clamp at 0
 }
 
-// Lower bound of d at config kO (R4): Alg. 1 never returns less than the largest
-// channel when every factor is >= 1 (each channel's isolated time is consumed at
-// rate 1/f <= 1 per unit of elapsed overlap), so T(F') >= max(C, NCCL, H2D, D2H).
+// Lower bound of one Alg. 1 row (R4, R5).  With every factor >= 1 each channel's
+// isolated time is consumed at rate 1/f <= 1 per unit of elapsed time, so
+// T >= max_j x_j (R4).  Tighter (R5): the first round lasts ov = min_j x_j F_j
+// over the nonzero pattern S and leaves channel m with x_m - ov/F_m, which takes
+// at least that long again, so T >= x_m + ov (1 - 1/F_m) for every m in S (and
+// T >= ov for the zero channels, which have g = 0 in the table).  Unit factors
+// make Alg. 1 the max itself, so only R4 is used there.
+template <bool UNIT>
+__device__ __forceinline__ double lb_row(double x0, double x1, double x2, double x3, const FGRow* FG) {
+    const double mx = dmax(dmax(x0, x1), dmax(x2, x3));
+    if (UNIT) return mx;
+    const unsigned pat = (unsigned)(x0 != 0.0) | ((unsigned)(x1 != 0.0) << 1) | ((unsigned)(x2 != 0.0) << 2) |
+                         ((unsigned)(x3 != 0.0) << 3);
+    if (__popc(pat) < 2) return mx;
+    const double2 r0 = FG[pat][0], r1 = FG[pat][1], r2 = FG[pat][2], r3 = FG[pat][3];
+    const double s0 = x0 * r0.x, s1 = x1 * r1.x, s2 = x2 * r2.x, s3 = x3 * r3.x;
+    double ov = (pat & 1u) ? s0 : CUDART_INF;
+    ov = ((pat & 2u) && s1 < ov) ? s1 : ov;
+    ov = ((pat & 4u) && s2 < ov) ? s2 : ov;
+    ov = ((pat & 8u) && s3 < ov) ? s3 : ov;
+    const double b0 = fma(ov, 1.0 - r0.y, x0), b1 = fma(ov, 1.0 - r1.y, x1);
+    const double b2 = fma(ov, 1.0 - r2.y, x2), b3 = fma(ov, 1.0 - r3.y, x3);
+    return dmax(dmax(b0, b1), dmax(b2, b3));
+}
+
+// True when every F' row has nonzero H2D and D2H at kO = 0, i.e. the nonzero
+// pattern of the rows is the same for every kO of the run.
+__device__ __forceinline__ bool fp_pattern_fixed(const TupleConst& tc, const RunState& rs) {
+    bool ok = true;
+    if (tc.nl0 > 0.0) ok = ok && rs.FpH_L != 0.0 && rs.FpD_L0 != 0.0;
+    if (tc.nl1 > 0.0) ok = ok && rs.FpH_L != 0.0 && rs.FpD_L1 != 0.0;
+    if (tc.first) ok = ok && rs.FpH_E != 0.0 && rs.FpD_E != 0.0;
+    if (tc.last) ok = ok && rs.FpH_H != 0.0 && rs.FpD_H != 0.0;
+    return ok;
+}
+
+// Lower bound of d at config kO: rs.dbase + the lb_row of every F' row.
 // `scale` bounds the magnitudes summed, for a rounding margin.
+template <bool UNIT>
 __device__ __forceinline__ double d_lower_bound(const TupleConst& tc, const RunState& rs, double kO,
-                                                double& scale) {
+                                                const FGRow* FG, double& scale) {
     double lb = rs.dbase, sc = fabs(rs.dbase);
     const double H = rs.FpH_L + kO * tc.L.sOh;
     if (tc.nl0 > 0.0) {
-        const double m = dmax(dmax(tc.L.C_F, tc.L.N_Fp), dmax(H, rs.FpD_L0 + kO * tc.L.sOd));
+        const double m = lb_row<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, FG);
         lb += tc.nl0 * m; sc += tc.nl0 * m;
     }
     if (tc.nl1 > 0.0) {
-        const double m = dmax(dmax(tc.L.C_F, tc.L.N_Fp), dmax(H, rs.FpD_L1 + kO * tc.L.sOd));
+        const double m = lb_row<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, FG);
         lb += tc.nl1 * m; sc += tc.nl1 * m;
     }
     if (tc.first) {
-        const double m = dmax(dmax(tc.E.C_F, tc.E.N_Fp), dmax(rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd));
+        const double m = lb_row<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG);
         lb += m; sc += m;
     }
     if (tc.last) {
-        const double m = dmax(dmax(tc.H.C_F, tc.H.N_Fp), dmax(rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd));
+        const double m = lb_row<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG);
         lb += m; sc += m;
     }
     scale = sc;
@@ -353,6 +408,26 @@ __device__ __forceinline__ u64 splitmix64(u64 x) {
 // ---------------------------------------------------------------------------
 
 constexpr int kEvalThreads = 256;
+
+// Instrumented build (-DMIST_COUNTERS): per-thread event counters of the frontier
+// sweep, flushed to A.phases[1..4]: runs through run_backward, runs dropped at
+// their first config by the bound, configs whose d was evaluated, k0 scan steps.
+#ifdef MIST_COUNTERS
+#define MIST_CTR(i, v) (ctr[i] += (v))
+#else
+#define MIST_CTR(i, v) ((void)0)
+#endif
+
+__device__ __forceinline__ void flush_ctr(const EvalArgs& A, const unsigned* ctr, unsigned lane) {
+#ifdef MIST_COUNTERS
+    if (!A.phases) return;
+    for (int i = 0; i < 4; ++i) {
+        unsigned v = ctr[i];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(A.phases + 1 + i, (u64)v);
+    }
+#endif
+}
 
 // O10 "p beats q" on (x, y, idx)
 __device__ __forceinline__ bool beats(double tp, double yp, u64 ip, double tq, double yq, u64 iq) {
@@ -403,7 +478,8 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
                                                 const UnitState& us, unsigned kW, unsigned kG, unsigned kA,
                                                 unsigned radix, double Q, int Q1, unsigned grp, const FGRow* FG,
                                                 bool cv, double ct, double cy, unsigned nrows, unsigned brows,
-                                                unsigned& nph, u64& fcnt, u64& fhash, const FiltView& fv) {
+                                                unsigned& nph, u64& fcnt, u64& fhash, const FiltView& fv,
+                                                unsigned* ctr) {
     // the staircase filter runs in the frontier sweep and in the pilot (both exact, O10)
     constexpr bool FILT = MODE == 0 || MODE == 2;
     const double dkW = kW, dkG = kG, dkA = kA;
@@ -422,6 +498,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
         // config is over budget has none: its t and d are never needed (R2).
         run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
         nph += brows;
+        MIST_CTR(0, 1);
         // Bound-and-skip (ykey = d): a config whose lower bound of d exceeds the
         // best d the run already has, or the y of a known feasible point with
         // t <= the run's t (pilot staircase / cached candidate, both with a
@@ -448,9 +525,14 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
         // (R2).  Starting every lane's evaluation loop there keeps the warp's F'
         // evaluations of kO_min in lockstep instead of serialising them.
         unsigned k0 = 0;
-        while (k0 + 1 < radix &&
-               !(mem_kO(tc, rs, (double)((MODE == 2) ? A.vals[k0] : k0), Q) <= tc.DMB))
-            ++k0;
+        if (MODE == 2) {
+            while (k0 + 1 < radix && !(mem_kO(tc, rs, (double)A.vals[k0], Q) <= tc.DMB)) {
+                ++k0;
+                MIST_CTR(3, 1);
+            }
+        } else {
+            k0 = first_feasible_kO(tc, rs, Q);
+        }
         if (MODE == 0 && A.fp)
             for (unsigned k = k0; k < radix; ++k) {
                 const u64 idx = idx0 + (u64)k * Q1;
@@ -464,15 +546,21 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             const u64 idx = idx0 + (u64)ko * Q1;
             if (FILT && !P.ykey) {
                 double scale;
-                const double lb = d_lower_bound(tc, rs, kO, scale);
+                const double lb = d_lower_bound<UNIT>(tc, rs, kO, FG, scale);
                 const double thr = best_y < y_thr ? best_y : y_thr;
                 if (lb - 1e-12 * scale > thr) {
                     if (A.fp) continue;                       // keep counting feasible configs
+                    // the bound is non-decreasing in kO while the F' nonzero pattern is fixed,
+                    // which holds for kO >= 1 (H2D and D2H grow with kO); at kO = 0 a zero
+                    // H2D or D2H channel switches the R5 factor row, so only skip that config
+                    if (!UNIT && ko == 0 && !fp_pattern_fixed(tc, rs)) continue;
+                    MIST_CTR(1, k == k0 ? 1u : 0u);
                     break;
                 }
             }
             // P13: the whole run shares t; keep its min (y, idx)
             if (!P.ykey) nph += nrows;
+            MIST_CTR(2, 1);
             const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, rs, kO, FG);
             if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
         }
@@ -540,6 +628,7 @@ k_eval(DevProblem P, EvalArgs A) {
                                (unsigned)(tc.last != 0);
         const unsigned brows = nrows * (tc.L.N_Bp != tc.L.N_B ? 2u : 1u);
         unsigned nph = active ? nrows : 0u;
+        unsigned ctr[4] = {0u, 0u, 0u, 0u};
         bool cv = false;                       // cached candidate
         double ct = 0.0, cy = 0.0, cm = 0.0;
         u64 ci = 0;
@@ -574,7 +663,7 @@ k_eval(DevProblem P, EvalArgs A) {
                     FiltView fv;
                     fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
                     const RunCand rc = frontier_run<UNIT, MODE>(P, A, tc, us, kW, kG, kA, radix, Q, Q1, grp, FG, cv,
-                                                                ct, cy, nrows, brows, nph, fcnt, fhash, fv);
+                                                                ct, cy, nrows, brows, nph, fcnt, fhash, fv, ctr);
                     has = rc.has; best_y = rc.y; best_i = rc.idx; best_m = rc.m; rs.t = rc.t;
                 }
                 if (MODE != 1 && has) {
@@ -601,6 +690,7 @@ k_eval(DevProblem P, EvalArgs A) {
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 if (lane == 0 && v) atomicAdd(A.phases, (u64)v);
             }
+            flush_ctr(A, ctr, lane);
             if (A.fp) {
                 // feasible-set fingerprint, warp-aggregated per group
                 const bool any = fcnt > 0;
@@ -648,6 +738,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
     const unsigned upt = A.upt;
     const u64 n_units = A.n_units;
     unsigned nph = 0;
+    unsigned ctr[4] = {0u, 0u, 0u, 0u};
     for (u64 base = (u64)blockIdx.x * NT; base < n_units; base += (u64)gridDim.x * NT) {
         const u64 last_unit = min(base + NT, n_units) - 1;
         const u64 tb0 = base / upt, tb1 = last_unit / upt;
@@ -733,7 +824,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                 const bool same = cv && cgrp == grp;
                 u64 fcnt = 0, fhash = 0;
                 const RunCand rc = frontier_run<UNIT, 0>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
-                                                         ct, cy, nrows, brows, nph, fcnt, fhash, fv);
+                                                         ct, cy, nrows, brows, nph, fcnt, fhash, fv, ctr);
                 if (A.fp && fcnt) {
                     atomicAdd(A.fp + 2 * (u64)grp, fcnt);
                     atomicAdd(A.fp + 2 * (u64)grp + 1, fhash);
@@ -761,7 +852,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0 && v) atomicAdd(A.phases, (u64)v);
-    }
+    }    flush_ctr(A, ctr, lane);
 }
 
 // Arbitrary index list (test hook): one thread per index, tuple built in registers.

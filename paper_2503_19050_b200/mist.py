@@ -20,6 +20,10 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmist.so")
+if os.environ.get("MIST_COUNTERS") == "1":   # instrumented build (python -m paper_2503_19050_b200.build --counters)
+    LIB_PATH = os.path.join(HERE, "libmist_counters.so")
+if os.environ.get("MIST_LIB"):                # A/B measurements against another build of the same ABI
+    LIB_PATH = os.environ["MIST_LIB"]
 MAX_SPLITS = 8
 NCCL_ID_BYTES = 128
 
