@@ -170,7 +170,7 @@ mist_status_t mist_nccl_unique_id(uint8_t id[MIST_NCCL_ID_BYTES]);
  * mist_pareto_frontier is called with t_end == 0 and a communicator.
  * Block-cyclic (SURVEY 8(e) "weight ranges if the measured imbalance exceeds a
  * few percent"): [0, n_tuples) is cut into nb = world*K blocks at
- * floor(n_tuples*i/nb), K = clamp(n_tuples/(world*2048), 1, 64), and rank r
+ * floor(n_tuples*i/nb), K = clamp(n_tuples/(world*2048), 1, 512), and rank r
  * owns blocks i = r (mod world); adjacent owned blocks are coalesced.  Every
  * tuple holds (Q+1)^4 configs, so shares are equal in configs to within one
  * tuple per block, and the per-tuple cost, which varies by orders of
@@ -268,6 +268,35 @@ mist_status_t mist_sample_frontier(const mist_point_t* frontier, const int64_t* 
                                    int64_t n_groups, const mist_group_t* groups, int32_t K,
                                    int64_t* picked, int64_t picked_cap, int64_t* n_picked,
                                    int64_t* picked_offsets);
+
+/* ---- a12 on the device -------------------------------
+ * Same operation as mist_sample_frontier (O11: alpha_j = j/(K-1), argmin over the
+ * group's frontier of alpha*G*t + (1-alpha)*y evaluated as ((alpha*G)*t) +
+ * ((1-alpha)*y) without contraction, ties to the smaller t then the smaller idx,
+ * distinct picks in order of first appearance), computed by one warp
+ * per group on the ctx device.
+ * frontier [n_points], group_offsets [n_groups+1] (group_offsets[0] = 0,
+ * group_offsets[n_groups] = n_points, non-decreasing): host or device memory,
+ * e.g. the outputs of mist_pareto_frontier with ykey = MIST_Y_DELTA.
+ * groups: host, n_groups entries (for G).  Outputs, host or device memory:
+ * picked[n_groups*K] = positions into `frontier` of group g's picks at
+ * picked[g*K .. g*K + n_picked[g]), -1 after them; n_picked[n_groups].
+ * INVALID_ARG for K < 2 or inconsistent offsets.  Synchronous. */
+mist_status_t mist_sample_frontier_gpu(mist_ctx_t* ctx, const mist_point_t* frontier, int64_t n_points,
+                                       const int64_t* group_offsets, int64_t n_groups,
+                                       const mist_group_t* groups, int32_t K, int64_t* picked,
+                                       int32_t* n_picked);
+/* Sweep + a12 in one call, for an MILP-only consumer: the
+ * (t, d) frontier is computed exactly as by mist_pareto_frontier(ykey =
+ * MIST_Y_DELTA) and sampled on the device; only the samples leave the GPU.
+ * out[n_groups*K]: group g's picks at out[g*K .. g*K + n_picked[g]) in pick
+ * order, padded with {idx = UINT64_MAX, t = y = mem = 0}; n_picked[n_groups].
+ * Host or device memory.  Multi-GPU as mist_pareto_frontier. */
+mist_status_t mist_pareto_sample(mist_ctx_t* ctx, const mist_model_t* model, int64_t global_batch,
+                                 const mist_mesh_t* mesh, const mist_space_t* space,
+                                 const mist_coeffs_t* coeffs, const mist_group_t* groups,
+                                 int64_t n_groups, uint64_t t_begin, uint64_t t_end, int32_t K,
+                                 mist_point_t* out, int32_t* n_picked);
 
 #ifdef __cplusplus
 }

@@ -43,6 +43,10 @@ cudaError_t launch_eval_at(cudaStream_t, int, const DevProblem&, const DevGroup*
 cudaError_t frontier_reduce(cudaStream_t, CandBuf, long long, SortScratch&, u32*, long long*, ReduceStats*);
 cudaError_t frontier_group_offsets(cudaStream_t, const u32*, long long, int, int64_t*);
 cudaError_t pack_points(cudaStream_t, CandBuf, long long, mist_point_t*);
+// from mist_sample_dev.cu
+cudaError_t sample_alpha(cudaStream_t, const double*, const double*, const unsigned long long*, int,
+                         const int64_t*, const double*, long long, int, int64_t*, int32_t*);
+cudaError_t gather_picks(cudaStream_t, const CandBuf&, const int64_t*, long long, mist_point_t*);
 long long scan_tmp_words(long long n);
 
 // ---------------------------------------------------------------------------
@@ -766,6 +770,49 @@ static mist_status_t merge_ranks(mist_ctx_t* ctx, long long nf_local, long long*
     return MIST_OK;
 }
 
+// a2-a11 of one mist_pareto_frontier / mist_pareto_sample call: this rank's
+// share (or [t_begin, t_end)), swept and reduced, merged across ranks; the
+// frontier is left sorted by (group, t) in ctx->cand, *nf records.
+static mist_status_t frontier_device(mist_ctx_t* ctx, const Prepared& pp, uint64_t t_begin, uint64_t t_end,
+                                     bool want_fp, long long* nf_out) {
+    mist_status_t st = MIST_OK;
+    u64 tb = t_begin, te = t_end;
+    std::vector<std::pair<u64, u64>> ranges;
+    if (te == 0) {
+        if (ctx->nccl && ctx->world > 1) {
+            for (auto& r : mist_shard_blocks(pp.total_tuples, ctx->rank, ctx->world)) ranges.push_back(r);
+        } else {
+            ranges.push_back({0, pp.total_tuples});
+        }
+    } else {
+        if (tb > te || te > pp.total_tuples) return fail(ctx, MIST_ERR_INVALID_ARG, "tuple range out of bounds");
+        ranges.push_back({tb, te});
+    }
+    u64 mine = 0;
+    for (auto& r : ranges) mine += r.second - r.first;
+    long long nf = 0;
+    if (mine > 0) {
+        st = sweep(ctx, pp, ranges, want_fp, &nf);
+        if (st != MIST_OK) return st;
+    } else {
+        CK(ensure(ctx->fp, sizeof(u64) * 2 * (size_t)pp.ng), "alloc fp");
+        CK(cudaMemsetAsync(ctx->fp.p, 0, sizeof(u64) * 2 * (size_t)pp.ng, ctx->stream), "zero fp");
+        st = ensure_cand(ctx, 4096);
+        if (st != MIST_OK) return st;
+    }
+    if (ctx->nccl && ctx->world > 1) {
+        st = merge_ranks(ctx, nf, &nf);
+        if (st != MIST_OK) return st;
+        if (want_fp) {
+            ncclResult_t r = ncclAllReduce(ctx->fp.p, ctx->fp.p, 2 * (size_t)pp.ng, ncclUint64, ncclSum,
+                                           (ncclComm_t)ctx->nccl, ctx->stream);
+            if (r != ncclSuccess) return fail(ctx, MIST_ERR_NCCL, std::string("ncclAllReduce fp: ") + ncclGetErrorString(r));
+        }
+    }
+    *nf_out = nf;
+    return MIST_OK;
+}
+
 extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_t* model, int64_t B,
                                               const mist_mesh_t* mesh, const mist_space_t* space,
                                               const mist_coeffs_t* coeffs, const mist_group_t* groups,
@@ -810,39 +857,9 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         ctx->stats.unit_factors = pp.P.unit_factors;
         ctx->stats.h2d_bytes = sizeof(DevGroup) * (uint64_t)pp.ng + sizeof(double) * 6 * (uint64_t)pp.P.n_b * pp.P.n_tp;
         int htot = ev_begin(ctx, CAT_TOTAL);   // inputs are resident in HBM from here on
-        u64 tb = t_begin, te = t_end;
-        std::vector<std::pair<u64, u64>> ranges;
-        if (te == 0) {
-            if (ctx->nccl && ctx->world > 1) {
-                for (auto& r : mist_shard_blocks(pp.total_tuples, ctx->rank, ctx->world)) ranges.push_back(r);
-            } else {
-                ranges.push_back({0, pp.total_tuples});
-            }
-        } else {
-            if (tb > te || te > pp.total_tuples) return fail(ctx, MIST_ERR_INVALID_ARG, "tuple range out of bounds");
-            ranges.push_back({tb, te});
-        }
-        u64 mine = 0;
-        for (auto& r : ranges) mine += r.second - r.first;
         long long nf = 0;
-        if (mine > 0) {
-            st = sweep(ctx, pp, ranges, want_fp, &nf);
-            if (st != MIST_OK) return st;
-        } else {
-            CK(ensure(ctx->fp, sizeof(u64) * 2 * (size_t)pp.ng), "alloc fp");
-            CK(cudaMemsetAsync(ctx->fp.p, 0, sizeof(u64) * 2 * (size_t)pp.ng, ctx->stream), "zero fp");
-            st = ensure_cand(ctx, 4096);
-            if (st != MIST_OK) return st;
-        }
-        if (ctx->nccl && ctx->world > 1) {
-            st = merge_ranks(ctx, nf, &nf);
-            if (st != MIST_OK) return st;
-            if (want_fp) {
-                ncclResult_t r = ncclAllReduce(ctx->fp.p, ctx->fp.p, 2 * (size_t)pp.ng, ncclUint64, ncclSum,
-                                               (ncclComm_t)ctx->nccl, ctx->stream);
-                if (r != ncclSuccess) return fail(ctx, MIST_ERR_NCCL, std::string("ncclAllReduce fp: ") + ncclGetErrorString(r));
-            }
-        }
+        st = frontier_device(ctx, pp, t_begin, t_end, want_fp, &nf);
+        if (st != MIST_OK) return st;
         // offsets + packed points
         CK(ensure(ctx->out, sizeof(mist_point_t) * (size_t)std::max<long long>(1, nf) +
                                 sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc out");
@@ -885,6 +902,99 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         if (fp_hash) CK(cudaMemcpy(fp_hash, hs.data(), sizeof(uint64_t) * ng, cudaMemcpyDefault), "copy fp");
     }
     ctx->cache_valid = 0;   // the cache only serves a retry after BUFFER_TOO_SMALL
+    return MIST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// a12 on the device
+// ---------------------------------------------------------------------------
+static mist_status_t stage_G(mist_ctx_t* ctx, const mist_group_t* groups, int64_t n_groups, double** d_G) {
+    std::vector<double> G((size_t)n_groups);
+    for (int64_t g = 0; g < n_groups; ++g) G[(size_t)g] = (double)groups[g].G;
+    CK(ensure(ctx->xfer, sizeof(double) * (size_t)n_groups + 256), "alloc G");
+    *d_G = (double*)ctx->xfer.p;
+    CK(cudaMemcpyAsync(*d_G, G.data(), sizeof(double) * (size_t)n_groups, cudaMemcpyHostToDevice, ctx->stream), "H2D G");
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_sample_frontier_gpu(mist_ctx_t* ctx, const mist_point_t* frontier, int64_t n_points,
+                                                  const int64_t* group_offsets, int64_t n_groups,
+                                                  const mist_group_t* groups, int32_t K, int64_t* picked,
+                                                  int32_t* n_picked) {
+    if (!ctx || K < 2 || n_groups < 1 || n_points < 0 || !group_offsets || !groups || !picked || !n_picked ||
+        (n_points > 0 && !frontier))
+        return fail(ctx, MIST_ERR_INVALID_ARG, "bad arguments");
+    CK(cudaSetDevice(ctx->device), "set device");
+    std::vector<int64_t> off((size_t)n_groups + 1);
+    CK(cudaMemcpy(off.data(), group_offsets, sizeof(int64_t) * off.size(), cudaMemcpyDefault), "read offsets");
+    if (off[0] != 0 || off[(size_t)n_groups] != n_points) return fail(ctx, MIST_ERR_INVALID_ARG, "offsets");
+    for (int64_t g = 0; g < n_groups; ++g)
+        if (off[(size_t)g + 1] < off[(size_t)g]) return fail(ctx, MIST_ERR_INVALID_ARG, "offsets not monotone");
+    // device staging: points, offsets, picks; G after them in xfer
+    const size_t pb = sizeof(mist_point_t) * (size_t)std::max<int64_t>(1, n_points);
+    const size_t ob = sizeof(int64_t) * off.size();
+    const size_t kb = sizeof(int64_t) * (size_t)n_groups * K, nb = sizeof(int32_t) * (size_t)n_groups;
+    CK(ensure(ctx->out, pb + ob + kb + nb + 64), "alloc staging");
+    char* base = (char*)ctx->out.p;
+    mist_point_t* d_pts = (mist_point_t*)base;
+    int64_t* d_off = (int64_t*)(base + pb);
+    int64_t* d_pick = (int64_t*)(base + pb + ob);
+    int32_t* d_np = (int32_t*)(base + pb + ob + kb);
+    if (n_points > 0)
+        CK(cudaMemcpyAsync(d_pts, frontier, pb, cudaMemcpyDefault, ctx->stream), "stage points");
+    CK(cudaMemcpyAsync(d_off, off.data(), ob, cudaMemcpyHostToDevice, ctx->stream), "stage offsets");
+    double* d_G = nullptr;
+    mist_status_t st = stage_G(ctx, groups, n_groups, &d_G);
+    if (st != MIST_OK) return st;
+    const double* pd = reinterpret_cast<const double*>(d_pts);
+    CK(sample_alpha(ctx->stream, pd + 1, pd + 2, reinterpret_cast<const unsigned long long*>(d_pts), 4, d_off, d_G,
+                    n_groups, K, d_pick, d_np), "sample");
+    CK(cudaMemcpyAsync(picked, d_pick, kb, cudaMemcpyDefault, ctx->stream), "copy picks");
+    CK(cudaMemcpyAsync(n_picked, d_np, nb, cudaMemcpyDefault, ctx->stream), "copy counts");
+    CK(cudaStreamSynchronize(ctx->stream), "sample sync");
+    return MIST_OK;
+}
+
+extern "C" mist_status_t mist_pareto_sample(mist_ctx_t* ctx, const mist_model_t* model, int64_t B,
+                                            const mist_mesh_t* mesh, const mist_space_t* space,
+                                            const mist_coeffs_t* coeffs, const mist_group_t* groups,
+                                            int64_t n_groups, uint64_t t_begin, uint64_t t_end, int32_t K,
+                                            mist_point_t* out, int32_t* n_picked) {
+    if (!ctx || K < 2 || !out || !n_picked) return fail(ctx, MIST_ERR_INVALID_ARG, "bad arguments");
+    CK(cudaSetDevice(ctx->device), "set device");
+    ctx->cache_valid = 0;
+    reset_stats(ctx);
+    Prepared pp;
+    mist_status_t st = prepare(ctx, model, B, mesh, space, coeffs, groups, n_groups, (int)MIST_Y_DELTA, &pp);
+    if (st != MIST_OK) return st;
+    ctx->stats.unit_factors = pp.P.unit_factors;
+    int htot = ev_begin(ctx, CAT_TOTAL);
+    long long nf = 0;
+    st = frontier_device(ctx, pp, t_begin, t_end, false, &nf);
+    if (st != MIST_OK) return st;
+    const size_t ob = sizeof(int64_t) * ((size_t)pp.ng + 1);
+    const size_t kb = sizeof(int64_t) * (size_t)pp.ng * K, nb = sizeof(int32_t) * (size_t)pp.ng;
+    const size_t qb = sizeof(mist_point_t) * (size_t)pp.ng * K;
+    CK(ensure(ctx->out, ob + kb + nb + qb + 64), "alloc sample");
+    char* base = (char*)ctx->out.p;
+    mist_point_t* d_q = (mist_point_t*)base;
+    int64_t* d_off = (int64_t*)(base + qb);
+    int64_t* d_pick = (int64_t*)(base + qb + ob);
+    int32_t* d_np = (int32_t*)(base + qb + ob + kb);
+    CK(frontier_group_offsets(ctx->stream, ctx->cand.group, nf, pp.ng, d_off), "offsets");
+    double* d_G = nullptr;
+    st = stage_G(ctx, groups, n_groups, &d_G);
+    if (st != MIST_OK) return st;
+    CK(sample_alpha(ctx->stream, ctx->cand.t, ctx->cand.y, ctx->cand.idx, 1, d_off, d_G, pp.ng, K, d_pick, d_np),
+       "sample");
+    CK(gather_picks(ctx->stream, ctx->cand, d_pick, (long long)pp.ng * K, d_q), "gather picks");
+    ctx->stats.kernel_launches += 3;
+    ev_end(ctx, htot);
+    CK(cudaMemcpyAsync(out, d_q, qb, cudaMemcpyDefault, ctx->stream), "copy samples");
+    CK(cudaMemcpyAsync(n_picked, d_np, nb, cudaMemcpyDefault, ctx->stream), "copy counts");
+    ctx->stats.d2h_bytes = qb + nb;
+    CK(cudaStreamSynchronize(ctx->stream), "final sync");
+    ev_flush(ctx);
     return MIST_OK;
 }
 

@@ -239,7 +239,7 @@ namespace {
 std::vector<std::pair<uint64_t, uint64_t>> shard_blocks(uint64_t n, int rank, int world) {
     const uint64_t W = (uint64_t)world;
     uint64_t K = n / (W * 2048);
-    K = std::max<uint64_t>(1, std::min<uint64_t>(64, K));
+    K = std::max<uint64_t>(1, std::min<uint64_t>(512, K));
     const uint64_t nb = W * K;
     std::vector<std::pair<uint64_t, uint64_t>> out;
     for (uint64_t i = (uint64_t)rank; i < nb; i += W) {

@@ -191,7 +191,7 @@ __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, dou
 
 // Per-unit state: the F phase of every block.
 struct UnitState {
-    double tf;                                  // sum over blocks of count * T(F)
+    double TF_L0, TF_L1, TF_E, TF_H;            // T(F) of each block (0 when absent)
     double FH_L, FH_E, FH_H;                    // F H2D = kW sWh
     double FD_L0, FD_L1, FD_E, FD_H;            // F D2H = kA sAd (r = 0 / 1 for layers)
 };
@@ -245,23 +245,32 @@ __device__ __forceinline__ unsigned first_feasible_kO(const TupleConst& tc, cons
 template <bool UNIT>
 __device__ __forceinline__ void unit_forward(const TupleConst& tc, double kW, double kA, const FGRow* FG,
                                              UnitState& us) {
-    double tf = 0.0;
     us.FH_L = kW * tc.L.sWh;
     us.FD_L0 = kA * tc.L.sAd;
     us.FD_L1 = kA * tc.L.sAd1;
-    if (tc.nl0 > 0.0) tf += tc.nl0 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L0, FG);
-    if (tc.nl1 > 0.0) tf += tc.nl1 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L1, FG);
+    us.TF_L0 = us.TF_L1 = us.TF_E = us.TF_H = 0.0;
+    if (tc.nl0 > 0.0) us.TF_L0 = pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L0, FG);
+    if (tc.nl1 > 0.0) us.TF_L1 = pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L1, FG);
     if (tc.first) {
         us.FH_E = kW * tc.E.sWh;
         us.FD_E = kA * tc.E.sAd;
-        tf += pred_intf<UNIT>(tc.E.C_F, tc.E.N_F, us.FH_E, us.FD_E, FG);
+        us.TF_E = pred_intf<UNIT>(tc.E.C_F, tc.E.N_F, us.FH_E, us.FD_E, FG);
     }
     if (tc.last) {
         us.FH_H = kW * tc.H.sWh;
         us.FD_H = kA * tc.H.sAd;
-        tf += pred_intf<UNIT>(tc.H.C_F, tc.H.N_F, us.FH_H, us.FD_H, FG);
+        us.TF_H = pred_intf<UNIT>(tc.H.C_F, tc.H.N_F, us.FH_H, us.FD_H, FG);
     }
-    us.tf = tf;
+}
+
+// sum over blocks of count * T(F) (Eq. 5's forward part)
+__device__ __forceinline__ double unit_tf(const TupleConst& tc, const UnitState& us) {
+    double tf = 0.0;
+    if (tc.nl0 > 0.0) tf += tc.nl0 * us.TF_L0;
+    if (tc.nl1 > 0.0) tf += tc.nl1 * us.TF_L1;
+    if (tc.first) tf += us.TF_E;
+    if (tc.last) tf += us.TF_H;
+    return tf;
 }
 
 // B and B' of one block; returns T(B), writes T(B') - T(B)
@@ -304,23 +313,25 @@ __device__ __forceinline__ void run_backward(const TupleConst& tc, const UnitSta
         rs.FpH_H = us.FH_H + kG * tc.H.sGh;
         rs.FpD_H = us.FD_H + kW * tc.H.sWd;
     }
-    rs.t = (us.tf + tb) + tc.t_p2p;
-    rs.dbase = db - us.tf;
+    rs.t = (unit_tf(tc, us) + tb) + tc.t_p2p;
+    rs.dbase = db;                   // d = db + sum count * (T(F') - T(F)), block by block (Eq. 6)
 }
 
 // d of config kO of the run: first-microbatch forward F' of every block (Eq. 6).
 template <bool UNIT>
-__device__ __forceinline__ double d_kO(const TupleConst& tc, const RunState& rs, double kO, const FGRow* FG) {
+__device__ __forceinline__ double d_kO(const TupleConst& tc, const UnitState& us, const RunState& rs, double kO,
+                                       const FGRow* FG) {
+    // per-block differences T(F') - T(F): exactly 0 for a block whose F' equals its F
     double ds = rs.dbase;
     const double H = rs.FpH_L + kO * tc.L.sOh;
     if (tc.nl0 > 0.0)
-        ds += tc.nl0 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, FG);
+        ds += tc.nl0 * (pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, FG) - us.TF_L0);
     if (tc.nl1 > 0.0)
-        ds += tc.nl1 * pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, FG);
+        ds += tc.nl1 * (pred_intf<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, FG) - us.TF_L1);
     if (tc.first)
-        ds += pred_intf<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG);
+        ds += pred_intf<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG) - us.TF_E;
     if (tc.last)
-        ds += pred_intf<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG);
+        ds += pred_intf<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG) - us.TF_H;
     return ds > 0.0 ? ds : 0.0;                             // L25: clamp at 0
 }
 
@@ -360,28 +371,28 @@ __device__ __forceinline__ bool fp_pattern_fixed(const TupleConst& tc, const Run
     return ok;
 }
 
-// Lower bound of d at config kO: rs.dbase + the lb_row of every F' row.
+// Lower bound of d at config kO: rs.dbase + sum count * (lb_row(F') - T(F)) over the blocks.
 // `scale` bounds the magnitudes summed, for a rounding margin.
 template <bool UNIT>
-__device__ __forceinline__ double d_lower_bound(const TupleConst& tc, const RunState& rs, double kO,
-                                                const FGRow* FG, double& scale) {
+__device__ __forceinline__ double d_lower_bound(const TupleConst& tc, const UnitState& us, const RunState& rs,
+                                                double kO, const FGRow* FG, double& scale) {
     double lb = rs.dbase, sc = fabs(rs.dbase);
     const double H = rs.FpH_L + kO * tc.L.sOh;
     if (tc.nl0 > 0.0) {
         const double m = lb_row<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, FG);
-        lb += tc.nl0 * m; sc += tc.nl0 * m;
+        lb += tc.nl0 * (m - us.TF_L0); sc += tc.nl0 * (m + us.TF_L0);
     }
     if (tc.nl1 > 0.0) {
         const double m = lb_row<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, FG);
-        lb += tc.nl1 * m; sc += tc.nl1 * m;
+        lb += tc.nl1 * (m - us.TF_L1); sc += tc.nl1 * (m + us.TF_L1);
     }
     if (tc.first) {
         const double m = lb_row<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG);
-        lb += m; sc += m;
+        lb += m - us.TF_E; sc += m + us.TF_E;
     }
     if (tc.last) {
         const double m = lb_row<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG);
-        lb += m; sc += m;
+        lb += m - us.TF_H; sc += m + us.TF_H;
     }
     scale = sc;
     return lb;
@@ -546,7 +557,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             const u64 idx = idx0 + (u64)ko * Q1;
             if (FILT && !P.ykey) {
                 double scale;
-                const double lb = d_lower_bound<UNIT>(tc, rs, kO, FG, scale);
+                const double lb = d_lower_bound<UNIT>(tc, us, rs, kO, FG, scale);
                 const double thr = best_y < y_thr ? best_y : y_thr;
                 if (lb - 1e-12 * scale > thr) {
                     if (A.fp) continue;                       // keep counting feasible configs
@@ -561,7 +572,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             // P13: the whole run shares t; keep its min (y, idx)
             if (!P.ykey) nph += nrows;
             MIST_CTR(2, 1);
-            const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, rs, kO, FG);
+            const double y = P.ykey ? memD / tc.D : d_kO<UNIT>(tc, us, rs, kO, FG);
             if (y < best_y) { best_y = y; best_i = idx; best_m = memD; has = true; }
         }
     }
@@ -655,7 +666,7 @@ k_eval(DevProblem P, EvalArgs A) {
                         const double memD = mem_kO(tc, rs, kO, Q);
                         const u64 o = idx - A.lo;
                         if (A.t) A.t[o] = rs.t;
-                        if (A.d) A.d[o] = d_kO<UNIT>(tc, rs, kO, FG);
+                        if (A.d) A.d[o] = d_kO<UNIT>(tc, us, rs, kO, FG);
                         if (A.mem) A.mem[o] = memD / tc.D;
                         if (A.feas) A.feas[o] = memD <= tc.DMB;
                     }
@@ -729,11 +740,14 @@ k_eval_q(DevProblem P, EvalArgs A) {
     extern __shared__ double smem[];
     FGRow* FG = reinterpret_cast<FGRow*>(smem);
     TupleConst* sT = reinterpret_cast<TupleConst*>(smem + 128);
+    // per-unit forward state of the CTA's NT units (read by whichever lane runs a run of the unit)
+    UnitState* sU = reinterpret_cast<UnitState*>(sT + ((NT + A.upt - 1) / A.upt + 1));
     const int tid = threadIdx.x;
     load_fg(P, FG, tid);
     const double Q = P.Q;
     const int Q1 = P.Q1;
     const unsigned lane = tid & 31;
+    UnitState* wU = sU + (tid & ~31);
     const unsigned radix = (unsigned)Q1;
     const unsigned upt = A.upt;
     const u64 n_units = A.n_units;
@@ -758,12 +772,13 @@ k_eval_q(DevProblem P, EvalArgs A) {
         const unsigned jj = (unsigned)(u - (tb0 + tk) * (u64)upt);
         const bool active = u < n_units && jj < radix * radix;
         const unsigned kW = jj / radix, kA = jj - kW * radix;
-        UnitState us;
         unsigned g0 = radix;
         {
             const TupleConst& tc = sT[tk];
             if (active) {
+                UnitState us;
                 unit_forward<UNIT>(tc, (double)kW, (double)kA, FG, us);
+                wU[lane] = us;
                 nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
                        (unsigned)(tc.last != 0);
                 RunState rm;
@@ -774,6 +789,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                 if (!(tc.mG >= tc.gb_k)) g0 = 0;      // no kG-suffix property: every run is a task
             }
         }
+        __syncwarp();
         const unsigned cnt = active ? radix - g0 : 0u;
         unsigned incl = cnt;
 #pragma unroll
@@ -801,15 +817,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
             const unsigned o_kA = __shfl_sync(0xffffffffu, kA, own);
             const unsigned o_g0 = __shfl_sync(0xffffffffu, g0, own);
             const unsigned o_ex = __shfl_sync(0xffffffffu, excl, own);
-            UnitState ou;
-            ou.tf = __shfl_sync(0xffffffffu, us.tf, own);
-            ou.FH_L = __shfl_sync(0xffffffffu, us.FH_L, own);
-            ou.FH_E = __shfl_sync(0xffffffffu, us.FH_E, own);
-            ou.FH_H = __shfl_sync(0xffffffffu, us.FH_H, own);
-            ou.FD_L0 = __shfl_sync(0xffffffffu, us.FD_L0, own);
-            ou.FD_L1 = __shfl_sync(0xffffffffu, us.FD_L1, own);
-            ou.FD_E = __shfl_sync(0xffffffffu, us.FD_E, own);
-            ou.FD_H = __shfl_sync(0xffffffffu, us.FD_H, own);
+            const UnitState& ou = wU[own];
             bool emit = false;
             double et = 0.0, ey = 0.0, em = 0.0;
             u64 ei = 0;
@@ -882,7 +890,7 @@ __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int
         run_backward<UNIT>(tc, us, kW, kG, kA, FG, rs);
         const double memD = mem_kO(tc, rs, (double)kO, (double)P.Q);
         if (t) t[i] = rs.t;
-        if (d) d[i] = d_kO<UNIT>(tc, rs, (double)kO, FG);
+        if (d) d[i] = d_kO<UNIT>(tc, us, rs, (double)kO, FG);
         if (mem) mem[i] = memD / tc.D;
         if (feas) feas[i] = memD <= tc.DMB;
     }
@@ -962,7 +970,7 @@ static int eval_cfg() {
 template <bool UNIT, int NT, int MINB>
 static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     static_assert(NT == kEvalThreads, "eval_smem_bytes sizes the tuple region for kEvalThreads");
-    const size_t smem = eval_smem_bytes(A.upt);
+    const size_t smem = eval_smem_bytes(A.upt) + NT * sizeof(UnitState);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {

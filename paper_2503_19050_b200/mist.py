@@ -35,7 +35,8 @@ EXPORTED = ("mist_ctx_create", "mist_ctx_destroy", "mist_status_string", "mist_c
             "mist_ctx_stats", "mist_ctx_set_timing", "mist_nccl_unique_id", "mist_ctx_init_comm",
             "mist_shard_ranges",
             "mist_enumerate_space", "mist_eval_stage_costs", "mist_eval_stage_costs_at",
-            "mist_pareto_frontier", "mist_frontier_points", "mist_sample_frontier")
+            "mist_pareto_frontier", "mist_frontier_points", "mist_sample_frontier",
+            "mist_sample_frontier_gpu", "mist_pareto_sample")
 
 
 class MistError(RuntimeError):
@@ -121,6 +122,9 @@ def lib():
                   P(mist_group_t), C.c_int64]
         L.mist_eval_stage_costs.argtypes = common + [C.c_uint64, C.c_uint64, V, V, V, V]
         L.mist_eval_stage_costs_at.argtypes = common + [V, C.c_int64, V, V, V, V]
+        if hasattr(L, "mist_pareto_sample") or not os.environ.get("MIST_LIB"):   # older A/B builds lack a12-dev
+            L.mist_sample_frontier_gpu.argtypes = [V, V, C.c_int64, V, C.c_int64, P(mist_group_t), C.c_int32, V, V]
+            L.mist_pareto_sample.argtypes = common + [C.c_uint64, C.c_uint64, C.c_int32, V, V]
         L.mist_pareto_frontier.argtypes = common + [C.c_uint64, C.c_uint64, C.c_int, V, C.c_int64,
                                                     P(C.c_int64), V, V, V]
         L.mist_sample_frontier.argtypes = [V, V, C.c_int64, P(mist_group_t), C.c_int32, V, C.c_int64,
@@ -128,6 +132,8 @@ def lib():
         L.mist_frontier_points.argtypes = [V, V, V, C.c_int64, C.c_int64, V, C.c_int64, P(C.c_int64), V]
         for name in EXPORTED:
             if name not in ("mist_ctx_destroy", "mist_status_string", "mist_ctx_last_error"):
+                if os.environ.get("MIST_LIB") and not hasattr(L, name):
+                    continue
                 getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -355,3 +361,33 @@ def mist_sample_frontier(points: np.ndarray, offsets: np.ndarray, spec: Spec, K:
     if st != 0:
         raise MistError(st, "mist_sample_frontier")
     return picked[: n.value], poffs
+
+
+def mist_sample_frontier_gpu(ctx: Context, points, offsets, spec: Spec, K: int = 16):
+    """a12 on the device.  points/offsets: numpy (POINT_DTYPE / int64) or CUDA
+    tensors.  Returns (picked[n_groups, K] int64 positions, -1 padded;
+    n_picked[n_groups] int32) as numpy arrays."""
+    ng = spec.n_groups
+    if isinstance(points, np.ndarray):
+        points = np.ascontiguousarray(points, dtype=POINT_DTYPE)
+        npts = len(points)
+    else:
+        npts = points.numel() // 4
+    if isinstance(offsets, np.ndarray):
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    picked = np.zeros((ng, K), dtype=np.int64)
+    npk = np.zeros(ng, dtype=np.int32)
+    st = lib().mist_sample_frontier_gpu(ctx.handle, _ptr(points), npts, _ptr(offsets), ng, spec.groups, K,
+                                        _ptr(picked), _ptr(npk))
+    ctx.check(st, "mist_sample_frontier_gpu")
+    return picked, npk
+
+
+def mist_pareto_sample(ctx: Context, spec: Spec, K: int = 16, t_begin: int = 0, t_end: int = 0):
+    """Sweep + device a12: returns (samples[n_groups, K] POINT_DTYPE, n_picked[n_groups])."""
+    ng = spec.n_groups
+    out = np.zeros(ng * K, dtype=POINT_DTYPE)
+    npk = np.zeros(ng, dtype=np.int32)
+    st = lib().mist_pareto_sample(ctx.handle, *spec.args(), t_begin, t_end, K, _ptr(out), _ptr(npk))
+    ctx.check(st, "mist_pareto_sample")
+    return out.reshape(ng, K), npk

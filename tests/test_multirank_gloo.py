@@ -102,8 +102,8 @@ def test_shard_ranges_cover_exactly():
             assert max(sizes) - min(sizes) <= nblk   # equal within one tuple per block
             if w == 1:
                 assert parts[0] == [(0, n)]
-    # block-cyclic: at cfg5 scale every rank of 8 gets 64 blocks spread over the whole range
+    # block-cyclic: at cfg5 scale every rank of 8 gets 512 blocks spread over the whole range
     p = mist.mist_shard_ranges(27496640, 3, 8)
-    assert len(p) == 64 and p[0][0] < 27496640 // 16 and p[-1][1] > 27496640 * 15 // 16
+    assert len(p) == 512 and p[0][0] < 27496640 // 16 and p[-1][1] > 27496640 * 15 // 16
     with pytest.raises(mist.MistError):
         mist.mist_shard_ranges(10, 2, 2)
