@@ -252,6 +252,14 @@ def main():
         ops = alg_ops(int(stats["phases_evaluated"]), my_configs, bool(stats["unit_factors"]))
         achieved = ops / (stats["eval_ms"] / 1e3) / 1e12
         peak = FP64_PEAK_OPS / 1e12
+        # inter-stage consumer (Eq. 2-3): host solve over the exact
+        # frontiers of the last step, outside the timed region
+        ts = time.perf_counter()
+        plan = mist.mist_solve_inter(spec.groups, pts, offs, pb.model.L, pb.N * pb.M)
+        solve_ms = (time.perf_counter() - ts) * 1e3
+        plan_line = {"solve_ms": solve_ms, "sweep_to_plan_ms": dev_total_ms / args.steps + solve_ms,
+                     "G": plan["G"], "S": plan["S"], "objective_s": plan["objective"],
+                     "candidates": "exact (t, d) frontiers", "host_threads": os.cpu_count()}
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline_sample(pb, budget_s=12.0)
@@ -277,6 +285,7 @@ def main():
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(stats["h2d_bytes"]),
                     "d2h_bytes_per_step": int(stats["d2h_bytes"])},
             "gpu_launches": launches,
+            "plan": plan_line,
             "clocks": clk,
             "stats_last_step": {k: stats[k] for k in ("candidates", "reductions", "sort_keys", "sort_passes",
                                                      "chunks", "precompute_ms", "reduce_ms", "merge_ms",

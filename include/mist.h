@@ -298,6 +298,41 @@ mist_status_t mist_pareto_sample(mist_ctx_t* ctx, const mist_model_t* model, int
                                  int64_t n_groups, uint64_t t_begin, uint64_t t_end, int32_t K,
                                  mist_point_t* out, int32_t* n_picked);
 
+/* ---- inter-stage consumer (Eq. 2-3)
+ * Host-only.  Chooses G, the number of stages S and, per stage i = 1..S, a group
+ * (the IntraStagePareto key (G, [i=1], [i=S], min(G, S-i+1), l_i, n_i, m_i), O2) and
+ * one of its candidate points, with sum l_i = num_layers and sum n_i*m_i =
+ * n_devices, minimising Eq. 2:
+ *     (G-1) max_i t_i + sum_i t_i + max_i (d_i - sum_{j<i} t_j)   (reading L4).
+ * Exact over the given candidates (label-setting DP); the objective
+ * is non-decreasing in every t_i and d_i, so passing each group's (t, d) frontier
+ * (mist_pareto_frontier with MIST_Y_DELTA) gives the optimum over the whole
+ * configuration space, and passing the alpha-samples (mist_sample_frontier /
+ * mist_pareto_sample) gives the paper's sampled formulation (Eq. 3).
+ * groups[n_groups]: the enumeration's group table; points + group_offsets
+ * [n_groups+1]: group g's candidates at points[group_offsets[g] ..
+ * group_offsets[g+1]), y = d.  All host memory.  n_threads <= 0: one per core
+ * (the G values are independent).
+ * plan: stage i's group index plan->group[i-1] and candidate position (into
+ * points) plan->point[i-1]; objective and its three terms recomputed from
+ * the chosen points in Eq. 2's order.  Ties: the first G (ascending), then the
+ * fewest stages.
+ * Errors: INVALID_ARG (null pointers, n_groups < 1, num_layers < 1, n_devices < 1,
+ * non-monotone offsets, a key field out of range); EMPTY_SPACE (no complete plan
+ * has a candidate at every stage); BUFFER_TOO_SMALL (S > MIST_MAX_STAGES). */
+#define MIST_MAX_STAGES 128
+typedef struct {
+    int32_t G, S;
+    double objective;            /* Eq. 2, s */
+    double t_max, t_sum, d_term; /* max_i t_i, sum_i t_i, max_i (d_i - sum_{j<i} t_j) */
+    int64_t labels;              /* DP labels kept, summed over G (diagnostic) */
+    int32_t group[MIST_MAX_STAGES];
+    int64_t point[MIST_MAX_STAGES];
+} mist_plan_t;
+mist_status_t mist_solve_inter(const mist_group_t* groups, int64_t n_groups, const mist_point_t* points,
+                               const int64_t* group_offsets, int32_t num_layers, int32_t n_devices,
+                               int32_t n_threads, mist_plan_t* plan);
+
 #ifdef __cplusplus
 }
 #endif

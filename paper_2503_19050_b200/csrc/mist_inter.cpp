@@ -1,0 +1,288 @@
+// mist_inter.cpp -- inter-stage consumer of the frontiers.
+//
+// Paper: Eq. 2-3: choose G, the number of stages S,
+// and per stage i a layer count l_i, a submesh (n_i, m_i) and a point f_i of
+// IntraStagePareto(i, l_i, (n_i, m_i)) minimising
+//     (G-1) max_i t_i + sum_i t_i + max_i (d_i - sum_{j<i} t_j)      (reading L4)
+// subject to sum l_i = L and sum n_i m_i = N*M.  The paper solves an
+// MILP with CBC; this is an exact label-setting dynamic program instead
+// (DESIGN.md 8), host C++, since the MILP is a host-side consumer of the
+// frontiers and not the optimisation target (BASELINE north_star).
+//
+// Rewriting the objective with suffix sums s_i = sum_{j>=i} t_j:
+//     sum_i t_i + max_i (d_i - sum_{j<i} t_j) = max_i (d_i + s_i),
+// so a partial plan of the LAST k stages is summarised by the label
+// (Ssum = s_{S-k+1}, Mx = max over its stages of d_i + s_i, Tm = max t_i), and
+// prepending a stage (t, d) gives (Ssum + t, max(Mx, d + Ssum + t), max(Tm, t)),
+// monotone in every component.  A label that another label of the same state
+// (layers used, devices used, k) matches or beats in all three can therefore
+// never lead to a better plan, and a label whose (G-1) Tm + Mx already reaches
+// the incumbent cannot either.  Stage i's group key depends on its distance from
+// the end (w = min(G, S-i+1), last = [i = S], O2), so building plans from the
+// last stage backwards lets one DP per G serve every S: closing the plan with a
+// "first" stage at step k gives S = k.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <limits>
+#include <map>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "mist.h"
+
+namespace {
+
+struct Label {
+    double S, M, T;      // suffix sum of t, max_i (d_i + s_i), max t_i
+    int32_t parent;      // node of the partial plan this extends (-1: empty)
+    int32_t g, p;        // this stage: group, candidate position within the group
+};
+
+struct Node {
+    int32_t parent, g, p;
+};
+
+struct State {
+    std::vector<Label> v;
+    size_t thr = 4096;      // filter again once v has grown past this
+};
+
+struct Result {
+    double val = std::numeric_limits<double>::infinity();
+    int32_t G = 0, S = 0;
+    std::vector<int32_t> g;   // stage 1..S
+    std::vector<int32_t> p;
+    int64_t labels = 0;
+};
+
+inline uint64_t pack_key(int G, int first, int last, int w, int l, int n, int m) {
+    // G <= 2^20, w, l <= 2^10, n, m <= 2^10
+    return ((uint64_t)G << 42) | ((uint64_t)first << 41) | ((uint64_t)last << 40) | ((uint64_t)w << 30) |
+           ((uint64_t)l << 20) | ((uint64_t)n << 10) | (uint64_t)m;
+}
+
+struct Problem {
+    const mist_group_t* groups;
+    const mist_point_t* pts;
+    const int64_t* offs;
+    int L, devices;
+    std::unordered_map<uint64_t, int32_t> key;     // group key -> index (non-empty groups only)
+    std::vector<std::pair<int, int>> meshes;       // distinct (n, m)
+
+    int32_t find(int G, int first, int last, int w, int l, int n, int m) const {
+        auto it = key.find(pack_key(G, first, last, w, l, n, m));
+        return it == key.end() ? -1 : it->second;
+    }
+};
+
+// Keep the labels of one state that no other label matches or beats in (T, S, M);
+// drop labels whose bound reaches the incumbent.  Sorted by (T, S, M); a staircase
+// over (S -> min M) of the labels kept so far answers "is there one with S' <= S
+// and M' <= M".
+void pareto_filter(std::vector<Label>& v, double G1, double inc) {
+    std::sort(v.begin(), v.end(), [](const Label& a, const Label& b) {
+        if (a.T != b.T) return a.T < b.T;
+        if (a.S != b.S) return a.S < b.S;
+        if (a.M != b.M) return a.M < b.M;
+        if (a.parent != b.parent) return a.parent < b.parent;
+        if (a.g != b.g) return a.g < b.g;
+        return a.p < b.p;
+    });
+    std::map<double, double> stair;   // S ascending, M strictly decreasing
+    size_t out = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+        const Label& a = v[i];
+        if (G1 * a.T + a.M >= inc) continue;
+        auto it = stair.upper_bound(a.S);
+        if (it != stair.begin()) {
+            auto pv = std::prev(it);
+            if (pv->second <= a.M) continue;        // matched or beaten
+        }
+        // entries with S'' >= S and M'' >= M are covered by this one for later queries
+        auto jt = stair.lower_bound(a.S);
+        while (jt != stair.end() && jt->second >= a.M) jt = stair.erase(jt);
+        stair[a.S] = a.M;
+        v[out++] = a;
+    }
+    v.resize(out);
+}
+
+// The DP of one G.  Plans whose value does not beat `inc` are not reported.
+Result solve_G(const Problem& pb, int G, double inc) {
+    Result best;
+    best.val = inc;
+    const double G1 = (double)(G - 1);
+    const int L = pb.L, D = pb.devices;
+    const int Smax = std::min(L, D);
+    std::vector<Node> nodes;
+    // states of step k: (layers used, devices used) -> labels
+    std::map<std::pair<int, int>, State> cur, nxt;
+    cur[{0, 0}].v.push_back(Label{0.0, 0.0, 0.0, -1, -1, -1});
+    int32_t close_parent = -1, close_g = -1, close_p = -1, close_k = 0;
+    for (int k = 1; k <= Smax && !cur.empty(); ++k) {
+        const int w = std::min(G, k), last = k == 1;
+        nxt.clear();
+        for (auto& st : cur) {
+            const int lu = st.first.first, du = st.first.second;
+            std::vector<Label>& labs = st.second.v;
+            // node ids of this state's labels (created once the labels survived filtering)
+            std::vector<int32_t> nid(labs.size());
+            for (size_t i = 0; i < labs.size(); ++i) {
+                if (labs[i].g < 0) { nid[i] = -1; continue; }
+                nid[i] = (int32_t)nodes.size();
+                nodes.push_back(Node{labs[i].parent, labs[i].g, labs[i].p});
+            }
+            const int lrem = L - lu, drem = D - du;
+            // close the plan: this stage is stage 1 (first) and S = k
+            for (auto& nm : pb.meshes) {
+                if (nm.first * nm.second != drem) continue;
+                const int32_t g = pb.find(G, 1, last, w, lrem, nm.first, nm.second);
+                if (g < 0) continue;
+                const int64_t a = pb.offs[g], b = pb.offs[g + 1];
+                for (size_t i = 0; i < labs.size(); ++i) {
+                    const Label& lb = labs[i];
+                    for (int64_t q = a; q < b; ++q) {
+                        const double t = pb.pts[q].t, d = pb.pts[q].y;
+                        const double S2 = lb.S + t, M2 = std::max(lb.M, d + S2), T2 = std::max(lb.T, t);
+                        const double val = G1 * T2 + M2;
+                        if (val < best.val) {
+                            best.val = val;
+                            close_parent = nid[i]; close_g = g; close_p = (int32_t)(q - a); close_k = k;
+                        }
+                    }
+                }
+            }
+            if (k == Smax) continue;
+            // extend: this stage is stage S-k+1 > 1; at least one layer and one device stay for the first
+            for (int l = 1; l <= lrem - 1; ++l)
+                for (auto& nm : pb.meshes) {
+                    const int sz = nm.first * nm.second;
+                    if (sz > drem - 1) continue;
+                    const int32_t g = pb.find(G, 0, last, w, l, nm.first, nm.second);
+                    if (g < 0) continue;
+                    const int64_t a = pb.offs[g], b = pb.offs[g + 1];
+                    State& ns = nxt[{lu + l, du + sz}];
+                    std::vector<Label>& out = ns.v;
+                    for (size_t i = 0; i < labs.size(); ++i) {
+                        const Label& lb = labs[i];
+                        if (G1 * lb.T + lb.M >= best.val) continue;
+                        for (int64_t q = a; q < b; ++q) {
+                            const double t = pb.pts[q].t, d = pb.pts[q].y;
+                            const double S2 = lb.S + t, M2 = std::max(lb.M, d + S2), T2 = std::max(lb.T, t);
+                            if (G1 * T2 + M2 >= best.val) continue;
+                            out.push_back(Label{S2, M2, T2, nid[i], g, (int32_t)(q - a)});
+                        }
+                    }
+                    if (out.size() > ns.thr) {
+                        pareto_filter(out, G1, best.val);
+                        ns.thr = 2 * out.size() + 4096;
+                    }
+                }
+        }
+        for (auto it = nxt.begin(); it != nxt.end();) {
+            pareto_filter(it->second.v, G1, best.val);
+            best.labels += (int64_t)it->second.v.size();
+            if (it->second.v.empty()) it = nxt.erase(it); else ++it;
+        }
+        std::swap(cur, nxt);
+    }
+    if (close_k > 0) {
+        best.G = G;
+        best.S = close_k;
+        best.g.push_back(close_g);
+        best.p.push_back(close_p);
+        for (int32_t nd = close_parent; nd >= 0; nd = nodes[nd].parent) {
+            best.g.push_back(nodes[nd].g);
+            best.p.push_back(nodes[nd].p);
+        }
+    }
+    return best;
+}
+
+}  // namespace
+
+extern "C" mist_status_t mist_solve_inter(const mist_group_t* groups, int64_t n_groups, const mist_point_t* points,
+                                          const int64_t* group_offsets, int32_t num_layers, int32_t n_devices,
+                                          int32_t n_threads, mist_plan_t* plan) {
+    if (!groups || n_groups < 1 || !group_offsets || !plan || num_layers < 1 || n_devices < 1)
+        return MIST_ERR_INVALID_ARG;
+    if (group_offsets[0] != 0) return MIST_ERR_INVALID_ARG;
+    for (int64_t g = 0; g < n_groups; ++g)
+        if (group_offsets[g + 1] < group_offsets[g]) return MIST_ERR_INVALID_ARG;
+    if (group_offsets[n_groups] > 0 && !points) return MIST_ERR_INVALID_ARG;
+    Problem pb;
+    pb.groups = groups; pb.pts = points; pb.offs = group_offsets;
+    pb.L = num_layers; pb.devices = n_devices;
+    std::vector<int> Gs;
+    for (int64_t g = 0; g < n_groups; ++g) {
+        const mist_group_t& gr = groups[g];
+        if (gr.G < 1 || gr.G >= (1 << 20) || gr.w < 1 || gr.w >= 1024 || gr.layers < 1 || gr.layers >= 1024 ||
+            gr.n < 1 || gr.n >= 1024 || gr.m < 1 || gr.m >= 1024)
+            return MIST_ERR_INVALID_ARG;
+        if (std::find(pb.meshes.begin(), pb.meshes.end(), std::make_pair(gr.n, gr.m)) == pb.meshes.end())
+            pb.meshes.push_back({gr.n, gr.m});
+        if (std::find(Gs.begin(), Gs.end(), gr.G) == Gs.end()) Gs.push_back(gr.G);
+        if (group_offsets[g + 1] > group_offsets[g])
+            pb.key[pack_key(gr.G, gr.first, gr.last, gr.w, gr.layers, gr.n, gr.m)] = (int32_t)g;
+    }
+    std::sort(pb.meshes.begin(), pb.meshes.end());
+    std::sort(Gs.begin(), Gs.end());
+
+    // incumbent seed: the best single-stage plan over every G (value G t + d, exact DP form)
+    double seed = std::numeric_limits<double>::infinity();
+    for (int G : Gs)
+        for (auto& nm : pb.meshes) {
+            if (nm.first * nm.second != n_devices) continue;
+            const int32_t g = pb.find(G, 1, 1, 1, num_layers, nm.first, nm.second);
+            if (g < 0) continue;
+            for (int64_t q = group_offsets[g]; q < group_offsets[g + 1]; ++q) {
+                const double t = points[q].t;
+                const double v = (double)(G - 1) * t + std::max(0.0, points[q].y + t);
+                seed = std::min(seed, v);
+            }
+        }
+    // the seed only prunes; a plan equal to it is found again by its own G's DP
+    const double inc = std::nextafter(seed, std::numeric_limits<double>::infinity());
+
+    std::vector<Result> res(Gs.size());
+    unsigned nt = n_threads > 0 ? (unsigned)n_threads : std::max(1u, std::thread::hardware_concurrency());
+    nt = std::min<unsigned>(nt, (unsigned)Gs.size());
+    std::atomic<size_t> next{0};
+    auto worker = [&]() {
+        for (size_t i; (i = next.fetch_add(1)) < Gs.size();) res[i] = solve_G(pb, Gs[i], inc);
+    };
+    std::vector<std::thread> th;
+    for (unsigned i = 1; i < nt; ++i) th.emplace_back(worker);
+    worker();
+    for (auto& t : th) t.join();
+
+    int best = -1;
+    int64_t labels = 0;
+    for (size_t i = 0; i < res.size(); ++i) {
+        labels += res[i].labels;
+        if (res[i].S > 0 && (best < 0 || res[i].val < res[best].val)) best = (int)i;   // ties: smaller G
+    }
+    if (best < 0) return MIST_ERR_EMPTY_SPACE;
+    const Result& r = res[best];
+    if (r.S > MIST_MAX_STAGES) return MIST_ERR_BUFFER_TOO_SMALL;
+    plan->G = r.G;
+    plan->S = r.S;
+    plan->labels = labels;
+    // Eq. 2 of the chosen plan, written out term by term (stage 1 = first)
+    double tmax = 0.0, tsum = 0.0, third = -std::numeric_limits<double>::infinity();
+    for (int i = 0; i < r.S; ++i) {
+        const mist_point_t& pt = points[group_offsets[r.g[i]] + r.p[i]];
+        third = std::max(third, pt.y - tsum);
+        tsum += pt.t;
+        tmax = std::max(tmax, pt.t);
+        plan->group[i] = r.g[i];
+        plan->point[i] = group_offsets[r.g[i]] + r.p[i];
+    }
+    plan->t_max = tmax;
+    plan->t_sum = tsum;
+    plan->d_term = third;
+    plan->objective = (double)(r.G - 1) * tmax + tsum + third;
+    return MIST_OK;
+}

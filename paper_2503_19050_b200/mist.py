@@ -36,7 +36,7 @@ EXPORTED = ("mist_ctx_create", "mist_ctx_destroy", "mist_status_string", "mist_c
             "mist_shard_ranges",
             "mist_enumerate_space", "mist_eval_stage_costs", "mist_eval_stage_costs_at",
             "mist_pareto_frontier", "mist_frontier_points", "mist_sample_frontier",
-            "mist_sample_frontier_gpu", "mist_pareto_sample")
+            "mist_sample_frontier_gpu", "mist_pareto_sample", "mist_solve_inter")
 
 
 class MistError(RuntimeError):
@@ -90,6 +90,15 @@ class mist_stats_t(C.Structure):
                 ("phases_evaluated", C.c_uint64)]
 
 
+MAX_STAGES = 128
+
+
+class mist_plan_t(C.Structure):
+    _fields_ = [("G", C.c_int32), ("S", C.c_int32), ("objective", C.c_double), ("t_max", C.c_double),
+                ("t_sum", C.c_double), ("d_term", C.c_double), ("labels", C.c_int64),
+                ("group", C.c_int32 * MAX_STAGES), ("point", C.c_int64 * MAX_STAGES)]
+
+
 POINT_DTYPE = np.dtype([("idx", "<u8"), ("t", "<f8"), ("y", "<f8"), ("mem", "<f8")])
 assert POINT_DTYPE.itemsize == C.sizeof(mist_point_t) == 32
 
@@ -130,6 +139,8 @@ def lib():
         L.mist_sample_frontier.argtypes = [V, V, C.c_int64, P(mist_group_t), C.c_int32, V, C.c_int64,
                                            P(C.c_int64), V]
         L.mist_frontier_points.argtypes = [V, V, V, C.c_int64, C.c_int64, V, C.c_int64, P(C.c_int64), V]
+        if hasattr(L, "mist_solve_inter"):
+            L.mist_solve_inter.argtypes = [V, C.c_int64, V, V, C.c_int32, C.c_int32, C.c_int32, P(mist_plan_t)]
         for name in EXPORTED:
             if name not in ("mist_ctx_destroy", "mist_status_string", "mist_ctx_last_error"):
                 if os.environ.get("MIST_LIB") and not hasattr(L, name):
@@ -391,3 +402,36 @@ def mist_pareto_sample(ctx: Context, spec: Spec, K: int = 16, t_begin: int = 0, 
     st = lib().mist_pareto_sample(ctx.handle, *spec.args(), t_begin, t_end, K, _ptr(out), _ptr(npk))
     ctx.check(st, "mist_pareto_sample")
     return out.reshape(ng, K), npk
+
+
+def group_array(keys) -> "C.Array":
+    """mist_group_t[] holding only the keys (G, first, last, w, l, n, m): the
+    part of the group table that mist_solve_inter reads."""
+    arr = (mist_group_t * len(keys))()
+    for i, k in enumerate(keys):
+        g = arr[i]
+        g.G, g.first, g.last, g.w, g.layers, g.n, g.m = (int(v) for v in k)
+    return arr
+
+
+def mist_solve_inter(groups, points: np.ndarray, offsets: np.ndarray, num_layers: int, n_devices: int,
+                     n_threads: int = 0) -> dict:
+    """Inter-stage plan (Eq. 2-3) over per-group candidates (CSR: points, offsets).
+    groups: a ctypes mist_group_t array (``Spec.groups`` or ``group_array``).
+    Returns dict(G, S, objective, t_max, t_sum, d_term, labels, group[S], point[S])."""
+    if points.dtype != POINT_DTYPE:            # e.g. records carrying extra fields
+        pts = np.zeros(len(points), dtype=POINT_DTYPE)
+        for f in POINT_DTYPE.names:
+            pts[f] = points[f]
+    else:
+        pts = np.ascontiguousarray(points)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    plan = mist_plan_t()
+    st = lib().mist_solve_inter(C.addressof(groups), len(groups), _ptr(pts) if len(pts) else None, _ptr(offs),
+                                int(num_layers), int(n_devices), int(n_threads), C.byref(plan))
+    if st != 0:
+        raise MistError(st, "mist_solve_inter")
+    S = plan.S
+    return dict(G=plan.G, S=S, objective=plan.objective, t_max=plan.t_max, t_sum=plan.t_sum,
+                d_term=plan.d_term, labels=plan.labels, group=np.array(plan.group[:S], dtype=np.int64),
+                point=np.array(plan.point[:S], dtype=np.int64))

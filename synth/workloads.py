@@ -249,3 +249,22 @@ def random_problem(seed: int) -> Problem:
 
 def to_dict(pb: Problem) -> Dict:
     return dataclasses.asdict(pb)
+
+
+def random_candidates(keys, seed: int, max_points: int = 3, p_empty: float = 0.15,
+                      scale: float = 1.0):
+    """Seeded per-group candidate tables for the inter-stage solver tests: for
+    each group key a staircase of 0..max_points (t, d) pairs (t ascending, d
+    descending, like a (t, d) frontier), with occasional repeated values.
+    Returns (points: list of (t, d) per group in key order)."""
+    rng = np.random.Generator(np.random.PCG64(SEED + 5000 + seed))
+    out = []
+    for _ in keys:
+        if rng.random() < p_empty:
+            out.append([])
+            continue
+        k = int(rng.integers(1, max_points + 1))
+        t = np.sort(rng.choice(np.arange(1, 40), size=k, replace=False)).astype(float) * scale
+        d = np.sort(rng.integers(0, 30, size=k))[::-1].astype(float) * scale
+        out.append([(float(a), float(b)) for a, b in zip(t, d)])
+    return out
