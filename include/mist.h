@@ -333,6 +333,34 @@ mist_status_t mist_solve_inter(const mist_group_t* groups, int64_t n_groups, con
                                const int64_t* group_offsets, int32_t num_layers, int32_t n_devices,
                                int32_t n_threads, mist_plan_t* plan);
 
+/* ---- interference model over observation tables -----
+ * Alg. 1 "Batched Interference Estimation" and the
+ * fitting of its slowdown factors, which the paper describes only as
+ * "data-driven ... the resulting runtime data is used to train the slowdown
+ * factors" (line 561).  Readings F1-F3.
+ * X: device memory, n rows of 4 doubles [C, NCCL, H2D, D2H] (the channel order
+ * of mist_coeffs_t.intf; Alg. 1's G2G = NCCL, C2G = H2D, G2C = D2H, L6),
+ * 32-byte aligned, every entry >= 0 and finite.  intf / init / out: the 16x4
+ * pattern-indexed factor table of mist_coeffs_t.intf (rows with < 2 bits
+ * ignored; member factors >= 1).
+ * mist_pred_intf: T[n] (device) = PredINTF of every row.
+ * mist_fit_intf: T_obs[n] (device, > 0) observed totals.  F1 loss = mean of
+ * ((PredINTF(X_i) - T_obs_i) / T_obs_i)^2; F2 coordinate descent over the 28
+ * member factors (pattern ascending, channel ascending), `iters` sweeps; F3 per
+ * coordinate 3 nested grids of 31 points over [1, fmax], each centred on the
+ * best value so far with half-width one previous step (lower end clamped at 1);
+ * a value replaces the current one only when its loss is strictly lower, so
+ * *loss never exceeds the loss of `init`.  out: fitted table (host), *loss:
+ * its loss.  Each grid level is ONE pass over the observations that evaluates
+ * all 32 candidates (one per lane).
+ * Errors: INVALID_ARG (null pointers, n < 1 for the fit, a member factor < 1,
+ * fmax <= 1, an invalid row or observation -- counted on the device, text in
+ * mist_ctx_last_error); CUDA.  Synchronous. */
+mist_status_t mist_pred_intf(mist_ctx_t* ctx, const double* X, int64_t n, const double intf[16][4], double* T);
+mist_status_t mist_fit_intf(mist_ctx_t* ctx, const double* X, const double* T_obs, int64_t n,
+                            const double init[16][4], int32_t iters, double fmax, double out[16][4],
+                            double* loss);
+
 #ifdef __cplusplus
 }
 #endif

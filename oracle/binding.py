@@ -84,6 +84,10 @@ def lib():
         P = C.POINTER
         L.orc_pred_intf.restype = C.c_double
         L.orc_pred_intf.argtypes = [P(C.c_double), P(C.c_double)]
+        L.orc_pred_intf_batch.restype = None
+        L.orc_pred_intf_batch.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.orc_intf_loss.restype = C.c_double
+        L.orc_intf_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_coll.restype = C.c_double
         L.orc_coll.argtypes = [P(ProblemS), C.c_int, C.c_double, C.c_int, C.c_int]
         L.orc_enumerate.argtypes = [P(ProblemS), P(Group), C.c_int64, P(C.c_int64), P(C.c_uint64)]
@@ -268,6 +272,22 @@ def pred_intf(X, F) -> float:
     x = (C.c_double * 4)(*X)
     f = (C.c_double * 64)(*[v for row in F for v in row])
     return lib().orc_pred_intf(x, f)
+
+
+def pred_intf_batch(X: np.ndarray, F) -> np.ndarray:
+    """Alg. 1 on every row of X[n][4] (literal routine, row by row)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    Fa = np.ascontiguousarray(F, dtype=np.float64).reshape(16, 4)
+    T = np.empty(len(X))
+    lib().orc_pred_intf_batch(_ptr(X), len(X), _ptr(Fa), _ptr(T))
+    return T
+
+
+def intf_loss(X: np.ndarray, Tobs: np.ndarray, F) -> float:
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    Tobs = np.ascontiguousarray(Tobs, dtype=np.float64)
+    Fa = np.ascontiguousarray(F, dtype=np.float64).reshape(16, 4)
+    return lib().orc_intf_loss(_ptr(X), _ptr(Tobs), len(X), _ptr(Fa))
 
 
 def frontier_points(points: np.ndarray, method: int = 0) -> np.ndarray:

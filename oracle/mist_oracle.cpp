@@ -76,6 +76,25 @@ extern "C" double orc_pred_intf(const double Xin[4], const double F[16][4]) {
     return T;
 }
 
+/* Alg. 1 over a batch of rows ("Batched Interference Estimation"):
+ * X[n][4] row-major, T[n] out.  Row by row, the literal routine above. */
+extern "C" void orc_pred_intf_batch(const double* X, int64_t n, const double F[16][4], double* T) {
+    for (int64_t i = 0; i < n; ++i) T[i] = orc_pred_intf(X + 4 * i, F);
+}
+
+/* Fitting loss ("the resulting runtime data is used to
+ * train the slowdown factors"; reading F1 in DESIGN.md 9): mean over the
+ * observations of the squared relative error ((PredINTF(X_i) - T_i) / T_i)^2,
+ * summed in row order. */
+extern "C" double orc_intf_loss(const double* X, const double* Tobs, int64_t n, const double F[16][4]) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double r = (orc_pred_intf(X + 4 * i, F) - Tobs[i]) / Tobs[i];
+        s += r * r;
+    }
+    return s / (double)n;
+}
+
 /* ------------------------------------------------------------------------ */
 /* O5 -- communication model (ring coefficients S:152, ledger L23).   */
 /* ------------------------------------------------------------------------ */

@@ -70,6 +70,8 @@ typedef struct {
 
 /* Alg. 1 PredINTF, literal. */
 double orc_pred_intf(const double X[4], const double F[16][4]);
+void orc_pred_intf_batch(const double* X, int64_t n, const double F[16][4], double* T);
+double orc_intf_loss(const double* X, const double* Tobs, int64_t n, const double F[16][4]);
 /* O5 collective time: kind 0=AR,1=AG,2=RS,3=P2P */
 double orc_coll(const orc_problem_t* pb, int kind, double bytes, int gsz, int inter);
 

@@ -36,7 +36,7 @@ EXPORTED = ("mist_ctx_create", "mist_ctx_destroy", "mist_status_string", "mist_c
             "mist_shard_ranges",
             "mist_enumerate_space", "mist_eval_stage_costs", "mist_eval_stage_costs_at",
             "mist_pareto_frontier", "mist_frontier_points", "mist_sample_frontier",
-            "mist_sample_frontier_gpu", "mist_pareto_sample", "mist_solve_inter")
+            "mist_sample_frontier_gpu", "mist_pareto_sample", "mist_solve_inter", "mist_pred_intf", "mist_fit_intf")
 
 
 class MistError(RuntimeError):
@@ -139,6 +139,9 @@ def lib():
         L.mist_sample_frontier.argtypes = [V, V, C.c_int64, P(mist_group_t), C.c_int32, V, C.c_int64,
                                            P(C.c_int64), V]
         L.mist_frontier_points.argtypes = [V, V, V, C.c_int64, C.c_int64, V, C.c_int64, P(C.c_int64), V]
+        if hasattr(L, "mist_fit_intf"):
+            L.mist_pred_intf.argtypes = [V, V, C.c_int64, V, V]
+            L.mist_fit_intf.argtypes = [V, V, V, C.c_int64, V, C.c_int32, C.c_double, V, P(C.c_double)]
         if hasattr(L, "mist_solve_inter"):
             L.mist_solve_inter.argtypes = [V, C.c_int64, V, V, C.c_int32, C.c_int32, C.c_int32, P(mist_plan_t)]
         for name in EXPORTED:
@@ -435,3 +438,31 @@ def mist_solve_inter(groups, points: np.ndarray, offsets: np.ndarray, num_layers
     return dict(G=plan.G, S=S, objective=plan.objective, t_max=plan.t_max, t_sum=plan.t_sum,
                 d_term=plan.d_term, labels=plan.labels, group=np.array(plan.group[:S], dtype=np.int64),
                 point=np.array(plan.point[:S], dtype=np.int64))
+
+
+def _table(F) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(F, dtype=np.float64).reshape(16, 4))
+
+
+def mist_pred_intf(ctx: Context, X, F, T=None):
+    """Alg. 1 on every row of X (CUDA tensor [n, 4] float64).  Returns T (CUDA tensor [n])."""
+    import torch
+    n = X.shape[0]
+    if T is None:
+        T = torch.empty(n, dtype=torch.float64, device=X.device)
+    tab = _table(F)
+    st = lib().mist_pred_intf(ctx.handle, _ptr(X), n, _ptr(tab), _ptr(T))
+    ctx.check(st, "mist_pred_intf")
+    return T
+
+
+def mist_fit_intf(ctx: Context, X, T_obs, init, iters: int = 2, fmax: float = 4.0):
+    """Fit the 28 member factors to observations (CUDA tensors X [n, 4], T_obs [n]).
+    Returns (table[16, 4] numpy, loss)."""
+    tab = _table(init)
+    out = np.zeros((16, 4), dtype=np.float64)
+    loss = C.c_double(0.0)
+    st = lib().mist_fit_intf(ctx.handle, _ptr(X), _ptr(T_obs), X.shape[0], _ptr(tab), int(iters), float(fmax),
+                             _ptr(out), C.byref(loss))
+    ctx.check(st, "mist_fit_intf")
+    return out, loss.value

@@ -268,3 +268,36 @@ def random_candidates(keys, seed: int, max_points: int = 3, p_empty: float = 0.1
         d = np.sort(rng.integers(0, 30, size=k))[::-1].astype(float) * scale
         out.append([(float(a), float(b)) for a, b in zip(t, d)])
     return out
+
+
+def random_factor_table(seed: int, lo: float = 1.0, hi: float = 2.0):
+    """Seeded 16x4 Alg. 1 factor table: every member factor uniform in [lo, hi]
+    (rows with < 2 channels and non-member entries are 1)."""
+    rng = np.random.Generator(np.random.PCG64(SEED + 7000 + seed))
+    F = [[1.0] * 4 for _ in range(16)]
+    for pat in range(16):
+        if bin(pat).count("1") < 2:
+            continue
+        for ch in range(4):
+            if pat >> ch & 1:
+                F[pat][ch] = float(rng.uniform(lo, hi))
+    return F
+
+
+def intf_rows(seed: int, n: int, min_channels: int = 1):
+    """Seeded channel vectors [C, NCCL, H2D, D2H] for the interference model:
+    a uniformly random non-empty channel subset of size >= min_channels per
+    row, each present channel log-uniform in [1e-4, 1e-1] s (the range of the
+    phase channels of the workloads)."""
+    rng = np.random.Generator(np.random.PCG64(SEED + 8000 + seed))
+    pats = [p for p in range(1, 16) if bin(p).count("1") >= min_channels]
+    pat = rng.choice(pats, size=n)
+    vals = 10.0 ** rng.uniform(-4.0, -1.0, size=(n, 4))
+    mask = ((pat[:, None] >> np.arange(4)[None, :]) & 1).astype(bool)
+    return np.where(mask, vals, 0.0)
+
+
+def noise(seed: int, n: int, rel: float):
+    """Seeded multiplicative noise factors uniform in [1 - rel, 1 + rel]."""
+    rng = np.random.Generator(np.random.PCG64(SEED + 9000 + seed))
+    return rng.uniform(1.0 - rel, 1.0 + rel, size=n)
