@@ -317,79 +317,6 @@ __device__ __forceinline__ void run_backward(const TupleConst& tc, const UnitSta
     rs.dbase = db;                   // d = db + sum count * (T(F') - T(F)), block by block (Eq. 6)
 }
 
-// Lazy variant for the frontier sweep (ykey = d, general factors): T(B) of every
-// block exactly (t needs it), but the last-microbatch rows B' only through the
-// R5 lower bound lb_row(B') (defined below), so rs.dbase is a LOWER BOUND of
-// sum count * (T(B') - T(B)).  The bound-and-skip test stays exact with it (it
-// only compares lower bounds); run_backward_exact_bp replaces it by the exact
-// value before the first d is evaluated.
-template <bool UNIT>
-__device__ __forceinline__ double lb_row(double x0, double x1, double x2, double x3, const FGRow* FG);
-
-__device__ __forceinline__ double block_backward_lazy(const BlockConst& b, bool r1, double FH, double kG, double kA,
-                                                      const FGRow* FG, double& dBp_lb) {
-    const double sAh = r1 ? b.sAh1 : b.sAh;
-    const double CB = r1 ? b.C_B1 : b.C_B;
-    const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
-    const double TB = pred_intf<false>(CB, b.N_B, BH, BD, FG);
-    // lb_row(B') - T(B) <= T(B') - T(B); clamp: T(B') >= T(B) is not assumed, the bound may be negative
-    dBp_lb = (b.N_Bp == b.N_B) ? 0.0 : lb_row<false>(CB, b.N_Bp, BH, BD, FG) - TB;
-    return TB;
-}
-
-__device__ __forceinline__ void run_backward_lazy(const TupleConst& tc, const UnitState& us, double kW, double kG,
-                                                  double kA, const FGRow* FG, RunState& rs) {
-    double tb = 0.0, db = 0.0, dBp;
-    rs.FpH_L = us.FH_L + kG * tc.L.sGh;
-    rs.FpD_L0 = us.FD_L0 + kW * tc.L.sWd;
-    rs.FpD_L1 = us.FD_L1 + kW * tc.L.sWd;
-    if (tc.nl0 > 0.0) {
-        tb += tc.nl0 * block_backward_lazy(tc.L, false, us.FH_L, kG, kA, FG, dBp);
-        db += tc.nl0 * dBp;
-    }
-    if (tc.nl1 > 0.0) {
-        tb += tc.nl1 * block_backward_lazy(tc.L, true, us.FH_L, kG, kA, FG, dBp);
-        db += tc.nl1 * dBp;
-    }
-    if (tc.first) {
-        tb += block_backward_lazy(tc.E, false, us.FH_E, kG, kA, FG, dBp);
-        db += dBp;
-        rs.FpH_E = us.FH_E + kG * tc.E.sGh;
-        rs.FpD_E = us.FD_E + kW * tc.E.sWd;
-    }
-    if (tc.last) {
-        tb += block_backward_lazy(tc.H, false, us.FH_H, kG, kA, FG, dBp);
-        db += dBp;
-        rs.FpH_H = us.FH_H + kG * tc.H.sGh;
-        rs.FpD_H = us.FD_H + kW * tc.H.sWd;
-    }
-    rs.t = (unit_tf(tc, us) + tb) + tc.t_p2p;
-    rs.dbase = db;
-}
-
-// The exact kO-independent part of d (as run_backward computes it, same order).
-__device__ __forceinline__ double run_dbase_exact(const TupleConst& tc, const UnitState& us, double kG, double kA,
-                                                  const FGRow* FG) {
-    double db = 0.0, dBp;
-    if (tc.nl0 > 0.0) {
-        block_backward<false>(tc.L, false, us.FH_L, kG, kA, FG, dBp);
-        db += tc.nl0 * dBp;
-    }
-    if (tc.nl1 > 0.0) {
-        block_backward<false>(tc.L, true, us.FH_L, kG, kA, FG, dBp);
-        db += tc.nl1 * dBp;
-    }
-    if (tc.first) {
-        block_backward<false>(tc.E, false, us.FH_E, kG, kA, FG, dBp);
-        db += dBp;
-    }
-    if (tc.last) {
-        block_backward<false>(tc.H, false, us.FH_H, kG, kA, FG, dBp);
-        db += dBp;
-    }
-    return db;
-}
-
 // d of config kO of the run: first-microbatch forward F' of every block (Eq. 6).
 template <bool UNIT>
 __device__ __forceinline__ double d_kO(const TupleConst& tc, const UnitState& us, const RunState& rs, double kO,
@@ -580,18 +507,8 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
         // D*mem is non-increasing in kO (O9: P_raw >= min(l,2) P_layer), so the
         // feasible configs of a run are a suffix in kO and a run whose kO = Q
         // config is over budget has none: its t and d are never needed (R2).
-        // frontier sweep with general factors: B' rows only through their lower bound
-        // until a config of the run survives the bound-and-skip test (lazy B')
-        constexpr bool LAZY = !UNIT && MODE == 0;
-        bool exact_bp = true;
-        if (LAZY && !P.ykey) {
-            run_backward_lazy(tc, us, dkW, dkG, dkA, FG, rs);
-            exact_bp = tc.L.N_Bp == tc.L.N_B;      // then every block's B' is its B
-            nph += nrows;
-        } else {
-            run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
-            nph += brows;
-        }
+        run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
+        nph += brows;
         MIST_CTR(0, 1);
         // Bound-and-skip (ykey = d): a config whose lower bound of d exceeds the
         // best d the run already has, or the y of a known feasible point with
@@ -651,11 +568,6 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
                     MIST_CTR(1, k == k0 ? 1u : 0u);
                     break;
                 }
-            }
-            if (LAZY && !exact_bp) {               // first surviving config: exact T(B') - T(B)
-                rs.dbase = run_dbase_exact(tc, us, dkG, dkA, FG);
-                exact_bp = true;
-                nph += nrows;
             }
             // P13: the whole run shares t; keep its min (y, idx)
             if (!P.ykey) nph += nrows;
