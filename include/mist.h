@@ -78,6 +78,12 @@ typedef struct {
     int32_t max_stages;          /* 0 => min(L, N*M) pipeline stages */
     int32_t n_grad_accum;        /* 0 => G over all divisors of B */
     const int32_t* grad_accum;   /* host, n_grad_accum entries */
+    /* Search-space presets (fig:search-space P:364-370,
+     * fig:eval-3-ablation P:810-822).  Zero = the full space.  A configuration
+     * outside the preset keeps its index (O3) but is never feasible, never
+     * fingerprinted and never on a frontier. */
+    int32_t ckpt_ends_only;      /* 1 => CKPT c in {0, l} only (no / full recomputation, Megatron-style) */
+    int32_t offload_off;         /* bit 0 WO, 1 GO, 2 OO, 3 AO: that ratio is fixed at 0 */
 } mist_space_t;
 
 /* Profiled coefficients: stand-in for the operator database (line 541) and
@@ -360,6 +366,15 @@ mist_status_t mist_pred_intf(mist_ctx_t* ctx, const double* X, int64_t n, const 
 mist_status_t mist_fit_intf(mist_ctx_t* ctx, const double* X, const double* T_obs, int64_t n,
                             const double init[16][4], int32_t iters, double fmax, double out[16][4],
                             double* loss);
+
+/* ---- search-space size (fig:search-space) ----
+ * Host-only.  *n_in_space = number of configurations of the space that the
+ * preset fields of `space` admit: sum over groups of n_splits * |ZeRO levels|
+ * * |CKPT choices| * prod over the four ratios of (1 if disabled else Q+1);
+ * |CKPT choices| = l+1, or 2 with ckpt_ends_only (l >= 1, so 0 != l).  *n_configs = the full index space (as mist_enumerate_space).
+ * Errors as mist_enumerate_space. */
+mist_status_t mist_count_space(const mist_model_t* model, int64_t global_batch, const mist_mesh_t* mesh,
+                               const mist_space_t* space, uint64_t* n_in_space, uint64_t* n_configs);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,7 @@ class ProblemS(C.Structure):
         ("bw", (C.c_double * 2) * 4), ("lat", (C.c_double * 2) * 4),
         ("bw_h2d", C.c_double), ("bw_d2h", C.c_double),
         ("intf", (C.c_double * 4) * 16),
+        ("ckpt_ends_only", C.c_int32), ("offload_off", C.c_int32),
     ]
 
 
@@ -86,6 +87,8 @@ def lib():
         L.orc_pred_intf.argtypes = [P(C.c_double), P(C.c_double)]
         L.orc_pred_intf_batch.restype = None
         L.orc_pred_intf_batch.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.orc_count_space.restype = C.c_uint64
+        L.orc_count_space.argtypes = [C.POINTER(ProblemS), C.POINTER(Group), C.c_int64]
         L.orc_intf_loss.restype = C.c_double
         L.orc_intf_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_coll.restype = C.c_double
@@ -127,6 +130,8 @@ class Oracle:
         s.model = Model(m.L, m.h, m.a, m.k, m.f, m.V, m.s, m.e, m.g, m.p, m.fl, m.nrm)
         s.B, s.N, s.M, s.mem_budget, s.Q = pb.B, pb.N, pb.M, pb.mem_budget, pb.Q
         s.zero_mask, s.max_stages = pb.zero_mask, pb.max_stages
+        s.ckpt_ends_only = int(getattr(pb, "ckpt_ends_only", 0))
+        s.offload_off = int(getattr(pb, "offload_off", 0))
         if pb.grad_accum:
             ga = np.asarray(pb.grad_accum, dtype=np.int32)
             self._keep.append(ga)
@@ -175,6 +180,10 @@ class Oracle:
         """(n_groups, 10) int64: G first last w l n m n_splits config_offset count"""
         return np.array([(g.G, g.first, g.last, g.w, g.l, g.n, g.m, g.n_splits, g.config_offset,
                           g.count) for g in self.groups], dtype=np.int64)
+
+    def count_space(self) -> int:
+        """Configurations the preset admits, counted one by one (small spaces)."""
+        return int(lib().orc_count_space(C.byref(self.s), self.groups, self.n_groups))
 
     def n_tuples(self) -> int:
         R = (self.pb.Q + 1) ** 4

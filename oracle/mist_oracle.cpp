@@ -280,6 +280,18 @@ struct CfgId {
     int split, z, c, kW, kG, kO, kA;
 };
 
+/* Search-space presets (fig:search-space P:364-370,
+ * fig:eval-3-ablation P:810-822): a configuration is in the preset unless it
+ * checkpoints a strict subset of the layers under ckpt_ends_only, or uses a
+ * nonzero ratio of a disabled offload type. */
+static bool in_preset(const orc_problem_t* pb, const CfgId& cf) {
+    if (pb->ckpt_ends_only && cf.c != 0 && cf.c != cf.g->l) return false;
+    const int k[4] = {cf.kW, cf.kG, cf.kO, cf.kA};
+    for (int r = 0; r < 4; ++r)
+        if ((pb->offload_off >> r & 1) && k[r] != 0) return false;
+    return true;
+}
+
 static int eval_config(const orc_problem_t* pb, const CfgId& cf, orc_detail_t* o) {
     const orc_model_t& md = pb->model;
     const orc_group_t& gr = *cf.g;
@@ -385,7 +397,27 @@ static int eval_config(const orc_problem_t* pb, const CfgId& cf, orc_detail_t* o
     o->mem_fwd_D = (double)fwd; o->mem_bwd_D = (double)bwd;
     o->mem = (double)Dmem / (double)D;
     o->feasible = Dmem <= (i128)pb->mem_budget * D;      /* max(Mem_fwd, Mem_bwd) <= Mem_Budget */
+    if (!in_preset(pb, cf)) o->feasible = 0;             /* outside the search-space preset */
     return 0;
+}
+
+/* Number of configurations a preset admits: counted one by one over every
+ * (group, split, z, c, kW, kG, kO, kA) -- small spaces only. */
+extern "C" uint64_t orc_count_space(const orc_problem_t* pb, const orc_group_t* groups, int64_t n_groups) {
+    const int nzl = num_zero_levels(pb);
+    uint64_t n = 0;
+    for (int64_t g = 0; g < n_groups; ++g)
+        for (int sp = 0; sp < groups[g].n_splits; ++sp)
+            for (int zi = 0; zi < nzl; ++zi)
+                for (int c = 0; c <= groups[g].l; ++c)
+                    for (int kW = 0; kW <= pb->Q; ++kW)
+                        for (int kG = 0; kG <= pb->Q; ++kG)
+                            for (int kO = 0; kO <= pb->Q; ++kO)
+                                for (int kA = 0; kA <= pb->Q; ++kA) {
+                                    CfgId cf = {&groups[g], sp, zero_level(pb, zi), c, kW, kG, kO, kA};
+                                    n += in_preset(pb, cf) ? 1 : 0;
+                                }
+    return n;
 }
 
 extern "C" int orc_eval_detail(const orc_problem_t* pb, const orc_group_t* grp, int split, int z,

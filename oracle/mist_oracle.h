@@ -40,6 +40,9 @@ typedef struct {
     double bw[4][2], lat[4][2];   /* [AR,AG,RS,P2P][intra,inter] */
     double bw_h2d, bw_d2h;
     double intf[16][4];           /* F[mask][channel], channels C,NCCL,H2D,D2H */
+    /* search-space preset: 0 = the full space */
+    int32_t ckpt_ends_only;       /* CKPT c in {0, l} only */
+    int32_t offload_off;          /* bit 0 WO, 1 GO, 2 OO, 3 AO fixed at ratio 0 */
 } orc_problem_t;
 
 typedef struct {
@@ -76,6 +79,7 @@ double orc_intf_loss(const double* X, const double* Tobs, int64_t n, const doubl
 double orc_coll(const orc_problem_t* pb, int kind, double bytes, int gsz, int inter);
 
 /* O2-O3 enumeration.  groups==NULL => size query. Returns 0 ok, <0 error. */
+uint64_t orc_count_space(const orc_problem_t* pb, const orc_group_t* groups, int64_t n_groups);
 int orc_enumerate(const orc_problem_t* pb, orc_group_t* groups, int64_t cap,
                   int64_t* n_groups, uint64_t* n_configs);
 

@@ -57,7 +57,8 @@ mist_status_t validate(const mist_model_t* model, int64_t B, const mist_mesh_t* 
     }
     if (!space || space->offload_steps < 1 || space->offload_steps > 1000 ||
         (space->zero_mask & 0xF) == 0 || (space->zero_mask & ~0xF) || space->max_stages < 0 ||
-        space->n_grad_accum < 0 || (space->n_grad_accum > 0 && !space->grad_accum)) {
+        space->n_grad_accum < 0 || (space->n_grad_accum > 0 && !space->grad_accum) ||
+        (space->ckpt_ends_only != 0 && space->ckpt_ends_only != 1) || (space->offload_off & ~0xF)) {
         *why = "invalid search space options"; return MIST_ERR_INVALID_ARG;
     }
     if (coeffs) {
@@ -99,6 +100,8 @@ void pack_problem(const mist_model_t* m, int64_t B, const mist_mesh_t* mesh,
         if (sp->zero_mask >> z & 1) P->zlev[P->nz++] = z;
     P->n_b = c->n_b; P->n_tp = c->n_tp;
     P->ykey = ykey;
+    P->ckpt_ends = sp->ckpt_ends_only;
+    for (int r = 0; r < 4; ++r) P->kmax[r] = (sp->offload_off >> r & 1) ? 0 : sp->offload_steps;
     P->B = B;
     P->mem_budget = mesh->mem_budget_bytes;
     std::memcpy(P->bw, c->bw, sizeof(P->bw));
@@ -231,6 +234,32 @@ extern "C" mist_status_t mist_enumerate_space(const mist_model_t* model, int64_t
     *n_configs = cfg;
     if (ng == 0) return MIST_ERR_EMPTY_SPACE;
     if (groups && ng > groups_cap) return MIST_ERR_BUFFER_TOO_SMALL;
+    return MIST_OK;
+}
+
+// Size of the preset space (fig:search-space P:364-370):
+// per group n_splits * |z| * |c| * prod(ratio counts), |c| = l + 1 or 2 (c in {0, l}).
+extern "C" mist_status_t mist_count_space(const mist_model_t* model, int64_t global_batch, const mist_mesh_t* mesh,
+                                          const mist_space_t* space, uint64_t* n_in_space, uint64_t* n_configs) {
+    if (!n_in_space || !n_configs) return MIST_ERR_INVALID_ARG;
+    int64_t ng = 0;
+    uint64_t nc = 0;
+    mist_status_t st = mist_enumerate_space(model, global_batch, mesh, space, nullptr, nullptr, 0, &ng, &nc);
+    if (st != MIST_OK) return st;
+    std::vector<mist_group_t> groups((size_t)ng);
+    st = mist_enumerate_space(model, global_batch, mesh, space, nullptr, groups.data(), ng, &ng, &nc);
+    if (st != MIST_OK) return st;
+    int nz = 0;
+    for (int z = 0; z < 4; ++z) nz += space->zero_mask >> z & 1;
+    uint64_t per_ratio = 1;
+    for (int r = 0; r < 4; ++r) per_ratio *= (space->offload_off >> r & 1) ? 1u : (uint64_t)space->offload_steps + 1;
+    uint64_t total = 0;
+    for (const mist_group_t& g : groups) {
+        const uint64_t nc_ckpt = space->ckpt_ends_only ? 2u : (uint64_t)g.layers + 1;
+        total += (uint64_t)g.n_splits * nz * nc_ckpt * per_ratio;
+    }
+    *n_in_space = total;
+    *n_configs = nc;
     return MIST_OK;
 }
 

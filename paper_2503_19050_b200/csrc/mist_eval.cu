@@ -131,6 +131,9 @@ __device__ void make_tuple(const DevProblem& P, const DevGroup* groups, int ng,
     o.DAx = c > 0 ? o.DA : 0.0;
     o.D = (double)Q * TP * DP;
     o.DMB = (double)P.mem_budget * o.D;
+    // preset: CKPT c in {0, l} only -- a tuple outside it is
+    // never feasible (every D*mem >= 0 > -1)
+    if (P.ckpt_ends && c != 0 && c != l) o.DMB = -1.0;
 }
 
 __global__ void k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ groups, int ng,
@@ -503,7 +506,10 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
     bool has = false;
     double best_y = CUDART_INF, best_m = 0.0;
     u64 best_i = 0;
-    if (mem_kO(tc, rs, Q, Q) <= tc.DMB) {
+    // preset: kO ranges over [0, kmax[2]] (pilot: the sub-grid values within it)
+    const unsigned kend = (MODE == 2) ? (P.kmax[2] == P.Q ? radix : 1u) : (unsigned)P.kmax[2] + 1u;
+    const double kOend = (MODE == 2) ? (double)A.vals[kend - 1] : (double)(kend - 1);
+    if (mem_kO(tc, rs, kOend, Q) <= tc.DMB) {
         // D*mem is non-increasing in kO (O9: P_raw >= min(l,2) P_layer), so the
         // feasible configs of a run are a suffix in kO and a run whose kO = Q
         // config is over budget has none: its t and d are never needed (R2).
@@ -537,7 +543,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
         // evaluations of kO_min in lockstep instead of serialising them.
         unsigned k0 = 0;
         if (MODE == 2) {
-            while (k0 + 1 < radix && !(mem_kO(tc, rs, (double)A.vals[k0], Q) <= tc.DMB)) {
+            while (k0 + 1 < kend && !(mem_kO(tc, rs, (double)A.vals[k0], Q) <= tc.DMB)) {
                 ++k0;
                 MIST_CTR(3, 1);
             }
@@ -545,11 +551,11 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             k0 = first_feasible_kO(tc, rs, Q);
         }
         if (MODE == 0 && A.fp)
-            for (unsigned k = k0; k < radix; ++k) {
+            for (unsigned k = k0; k < kend; ++k) {
                 const u64 idx = idx0 + (u64)k * Q1;
                 if (mem_kO(tc, rs, (double)k, Q) <= tc.DMB) { fcnt++; fhash += splitmix64(idx); }
             }
-        for (unsigned k = k0; k < radix; ++k) {
+        for (unsigned k = k0; k < kend; ++k) {
             const unsigned ko = (MODE == 2) ? A.vals[k] : k;
             const double kO = ko;
             const double memD = mem_kO(tc, rs, kO, Q);
@@ -625,10 +631,14 @@ k_eval(DevProblem P, EvalArgs A) {
         const u64 u = base + tid;
         const unsigned tk = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
         const unsigned jj = (unsigned)(u - (tb0 + tk) * (u64)upt);
-        const bool active = u < n_units && jj < radix * radix;
+        const bool unit_ok = u < n_units && jj < radix * radix;
         const unsigned iW = jj / radix, iA = jj - iW * radix;
-        const unsigned kW = (MODE == 2) ? A.vals[active ? iW : 0] : iW;
-        const unsigned kA = (MODE == 2) ? A.vals[active ? iA : 0] : iA;
+        const unsigned kW = (MODE == 2) ? A.vals[unit_ok ? iW : 0] : iW;
+        const unsigned kA = (MODE == 2) ? A.vals[unit_ok ? iA : 0] : iA;
+        // preset: a unit with kW or kA beyond its ratio's range has no configuration in
+        // the space (the dense mode still writes t, d, mem for it, with feasible = 0)
+        const bool in_unit = kW <= (unsigned)P.kmax[0] && kA <= (unsigned)P.kmax[3];
+        const bool active = unit_ok && (MODE == 1 || in_unit);
         const double dkW = kW, dkA = kA;
         const TupleConst& tc = sT[tk];
         const unsigned grp = tc.group;
@@ -648,8 +658,8 @@ k_eval(DevProblem P, EvalArgs A) {
             bool emit = false;
             double et = 0.0, ey = 0.0, em = 0.0;
             u64 ei = 0;
-            if (active) {
-                const unsigned kG = (MODE == 2) ? A.vals[ig] : ig;
+            const unsigned kG = (MODE == 2) ? A.vals[ig] : ig;
+            if (active && (MODE == 1 || kG <= (unsigned)P.kmax[1])) {
                 const double dkG = kG;
                 RunState rs;
                 run_memory(tc, dkW, dkG, dkA, Q, rs);
@@ -668,7 +678,9 @@ k_eval(DevProblem P, EvalArgs A) {
                         if (A.t) A.t[o] = rs.t;
                         if (A.d) A.d[o] = d_kO<UNIT>(tc, us, rs, kO, FG);
                         if (A.mem) A.mem[o] = memD / tc.D;
-                        if (A.feas) A.feas[o] = memD <= tc.DMB;
+                        if (A.feas)
+                            A.feas[o] = memD <= tc.DMB && in_unit && kG <= (unsigned)P.kmax[1] &&
+                                        k <= P.kmax[2];
                     }
                 } else {
                     FiltView fv;
@@ -770,8 +782,10 @@ k_eval_q(DevProblem P, EvalArgs A) {
         const u64 u = base + tid;
         const unsigned tk = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
         const unsigned jj = (unsigned)(u - (tb0 + tk) * (u64)upt);
-        const bool active = u < n_units && jj < radix * radix;
         const unsigned kW = jj / radix, kA = jj - kW * radix;
+        const bool active = u < n_units && jj < radix * radix && kW <= (unsigned)P.kmax[0] &&
+                            kA <= (unsigned)P.kmax[3];                   // preset ranges
+        const unsigned gend = (unsigned)P.kmax[1] + 1u;                  // runs kG < gend
         unsigned g0 = radix;
         {
             const TupleConst& tc = sT[tk];
@@ -782,15 +796,16 @@ k_eval_q(DevProblem P, EvalArgs A) {
                 nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
                        (unsigned)(tc.last != 0);
                 RunState rm;
-                for (unsigned ig = 0; ig < radix; ++ig) {
+                const double kOend = (double)P.kmax[2];
+                for (unsigned ig = 0; ig < gend; ++ig) {
                     run_memory(tc, (double)kW, (double)ig, (double)kA, Q, rm);
-                    if (mem_kO(tc, rm, Q, Q) <= tc.DMB) { g0 = ig; break; }
+                    if (mem_kO(tc, rm, kOend, Q) <= tc.DMB) { g0 = ig; break; }
                 }
                 if (!(tc.mG >= tc.gb_k)) g0 = 0;      // no kG-suffix property: every run is a task
             }
         }
         __syncwarp();
-        const unsigned cnt = active ? radix - g0 : 0u;
+        const unsigned cnt = (active && g0 < gend) ? gend - g0 : 0u;
         unsigned incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -892,7 +907,9 @@ __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int
         if (t) t[i] = rs.t;
         if (d) d[i] = d_kO<UNIT>(tc, us, rs, (double)kO, FG);
         if (mem) mem[i] = memD / tc.D;
-        if (feas) feas[i] = memD <= tc.DMB;
+        if (feas)
+            feas[i] = memD <= tc.DMB && kW <= (unsigned)P.kmax[0] && kG <= (unsigned)P.kmax[1] &&
+                      kO <= (unsigned)P.kmax[2] && kA <= (unsigned)P.kmax[3];
     }
 }
 

@@ -30,6 +30,8 @@ struct DevProblem {
     int n_b, n_tp;
     int ykey;
     int unit_factors;          // all Alg. 1 factors == 1
+    int ckpt_ends;             // preset: CKPT c in {0, l} only
+    int kmax[4];               // preset: largest admitted kW, kG, kO, kA (0 or Q)
     long long B;
     long long mem_budget;
     double bw[4][2], lat[4][2];

@@ -36,7 +36,7 @@ EXPORTED = ("mist_ctx_create", "mist_ctx_destroy", "mist_status_string", "mist_c
             "mist_shard_ranges",
             "mist_enumerate_space", "mist_eval_stage_costs", "mist_eval_stage_costs_at",
             "mist_pareto_frontier", "mist_frontier_points", "mist_sample_frontier",
-            "mist_sample_frontier_gpu", "mist_pareto_sample", "mist_solve_inter", "mist_pred_intf", "mist_fit_intf")
+            "mist_sample_frontier_gpu", "mist_pareto_sample", "mist_solve_inter", "mist_pred_intf", "mist_fit_intf", "mist_count_space")
 
 
 class MistError(RuntimeError):
@@ -57,7 +57,8 @@ class mist_mesh_t(C.Structure):
 
 class mist_space_t(C.Structure):
     _fields_ = [("offload_steps", C.c_int32), ("zero_mask", C.c_int32), ("max_stages", C.c_int32),
-                ("n_grad_accum", C.c_int32), ("grad_accum", C.POINTER(C.c_int32))]
+                ("n_grad_accum", C.c_int32), ("grad_accum", C.POINTER(C.c_int32)),
+                ("ckpt_ends_only", C.c_int32), ("offload_off", C.c_int32)]
 
 
 class mist_coeffs_t(C.Structure):
@@ -139,6 +140,9 @@ def lib():
         L.mist_sample_frontier.argtypes = [V, V, C.c_int64, P(mist_group_t), C.c_int32, V, C.c_int64,
                                            P(C.c_int64), V]
         L.mist_frontier_points.argtypes = [V, V, V, C.c_int64, C.c_int64, V, C.c_int64, P(C.c_int64), V]
+        if hasattr(L, "mist_count_space"):
+            L.mist_count_space.argtypes = [P(mist_model_t), C.c_int64, P(mist_mesh_t), P(mist_space_t),
+                                           P(C.c_uint64), P(C.c_uint64)]
         if hasattr(L, "mist_fit_intf"):
             L.mist_pred_intf.argtypes = [V, V, C.c_int64, V, V]
             L.mist_fit_intf.argtypes = [V, V, V, C.c_int64, V, C.c_int32, C.c_double, V, P(C.c_double)]
@@ -175,7 +179,8 @@ class Spec:
         self.model = mist_model_t(m.L, m.h, m.a, m.k, m.f, m.V, m.s, m.e, m.g, m.p, m.fl, m.nrm)
         self.B = int(pb.B)
         self.mesh = mist_mesh_t(pb.N, pb.M, int(pb.mem_budget))
-        self.space = mist_space_t(pb.Q, pb.zero_mask, pb.max_stages, 0, None)
+        self.space = mist_space_t(pb.Q, pb.zero_mask, pb.max_stages, 0, None,
+                                  int(getattr(pb, "ckpt_ends_only", 0)), int(getattr(pb, "offload_off", 0)))
         if pb.grad_accum:
             ga = np.ascontiguousarray(pb.grad_accum, dtype=np.int32)
             self._keep.append(ga)
@@ -466,3 +471,13 @@ def mist_fit_intf(ctx: Context, X, T_obs, init, iters: int = 2, fmax: float = 4.
                              _ptr(out), C.byref(loss))
     ctx.check(st, "mist_fit_intf")
     return out, loss.value
+
+
+def mist_count_space(spec: Spec) -> Tuple[int, int]:
+    """(configurations the preset admits, size of the full index space)."""
+    a, b = C.c_uint64(0), C.c_uint64(0)
+    st = lib().mist_count_space(C.byref(spec.model), spec.B, C.byref(spec.mesh), C.byref(spec.space),
+                                C.byref(a), C.byref(b))
+    if st != 0:
+        raise MistError(st, "mist_count_space")
+    return a.value, b.value

@@ -78,6 +78,8 @@ class Problem:
     Q: int                      # offload ratio steps (ratio grid k/Q)
     zero_mask: int = 0xF        # allowed ZeRO levels (bit z)
     max_stages: int = 0         # 0 => min(L, N*M)
+    ckpt_ends_only: int = 0     # preset: CKPT c in {0, l} only
+    offload_off: int = 0        # preset: bit 0 WO, 1 GO, 2 OO, 3 AO fixed at 0
     grad_accum: Optional[List[int]] = None   # None => all divisors of B
     profile: str = "L4"
     factors: str = "spec"       # unit | spec | asym
@@ -301,3 +303,24 @@ def noise(seed: int, n: int, rel: float):
     """Seeded multiplicative noise factors uniform in [1 - rel, 1 + rel]."""
     rng = np.random.Generator(np.random.PCG64(SEED + 9000 + seed))
     return rng.uniform(1.0 - rel, 1.0 + rel, size=n)
+
+
+# Nested search-space presets (SURVEY 8(f) rank 4; fig:search-space P:364-370 and
+# fig:eval-3-ablation P:810-822: Megatron-LM's space, then CKPT tuning, ZeRO,
+# offloading).  Reading S1 (DESIGN.md 10): "Megatron" = ZeRO 0, no or full
+# recomputation, no offloading.
+PRESETS = [
+    ("megatron", dict(zero_mask=0x1, ckpt_ends_only=1, offload_off=0xF)),
+    ("+ckpt", dict(zero_mask=0x1, ckpt_ends_only=0, offload_off=0xF)),
+    ("+zero", dict(zero_mask=0xF, ckpt_ends_only=0, offload_off=0xF)),
+    ("+offload", dict(zero_mask=0xF, ckpt_ends_only=0, offload_off=0x0)),
+]
+
+
+def with_preset(pb: Problem, name: str) -> Problem:
+    """A copy of pb restricted to preset `name` (inputs only)."""
+    q = copy.deepcopy(pb)
+    for k, v in dict(PRESETS)[name].items():
+        setattr(q, k, v)
+    q.name = f"{pb.name}[{name}]"
+    return q
