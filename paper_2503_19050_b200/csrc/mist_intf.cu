@@ -80,6 +80,8 @@ __device__ __forceinline__ double alg1(double x0, double x1, double x2, double x
     return T + (((x0 + x1) + x2) + x3);
 }
 
+constexpr int kPredRows = 4;   // rows per thread per iteration: their loads are issued together (MLP)
+
 __global__ void k_pred_intf(FactorTable tab, const double4* __restrict__ X, long long n, double* __restrict__ T) {
     __shared__ double sf[16][4], sg[16][4];
     if (threadIdx.x < 64) {
@@ -87,10 +89,19 @@ __global__ void k_pred_intf(FactorTable tab, const double4* __restrict__ X, long
         sg[threadIdx.x >> 2][threadIdx.x & 3] = tab.g[threadIdx.x >> 2][threadIdx.x & 3];
     }
     __syncthreads();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const double4 x = X[i];
-        T[i] = alg1(x.x, x.y, x.z, x.w, sf, sg, -1, -1, 1.0, 1.0);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n; i0 += stride * kPredRows) {
+        double4 x[kPredRows];
+#pragma unroll
+        for (int r = 0; r < kPredRows; ++r) {
+            const long long i = i0 + r * stride;
+            x[r] = i < n ? X[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+        }
+#pragma unroll
+        for (int r = 0; r < kPredRows; ++r) {
+            const long long i = i0 + r * stride;
+            if (i < n) T[i] = alg1(x[r].x, x[r].y, x[r].z, x[r].w, sf, sg, -1, -1, 1.0, 1.0);
+        }
     }
 }
 
@@ -148,12 +159,20 @@ k_fit_loss(FactorTable tab, const double4* __restrict__ X, const double* __restr
     }
 }
 
-// losses[k] = sum over blocks (fixed order) of partial[b][k] / n
+// losses[k] = sum over blocks of partial[b][k] / n: warp w sums blocks b = w (mod 8)
+// in order, then the 8 warp sums are added in warp order (deterministic)
 __global__ void k_fit_reduce(const double* __restrict__ partial, int nb, long long n, double* __restrict__ losses) {
-    const int k = threadIdx.x;
+    __shared__ double ws[8][32];
+    const int k = threadIdx.x & 31, w = threadIdx.x >> 5;
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += partial[(long long)b * 32 + k];
-    losses[k] = s / (double)n;
+    for (int b = w; b < nb; b += 8) s += partial[(long long)b * 32 + k];
+    ws[w][k] = s;
+    __syncthreads();
+    if (w == 0) {
+        double t = 0.0;
+        for (int v = 0; v < 8; ++v) t += ws[v][k];
+        losses[k] = t / (double)n;
+    }
 }
 
 int sm_count(int dev) {
@@ -242,7 +261,7 @@ extern "C" mist_status_t mist_fit_intf(mist_ctx_t* ctx, const double* X, const d
         cudaMemcpyAsync(dcand, cand.data(), 32 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
         k_fit_loss<<<(unsigned)nb, kFitThreads, 0, ctx->stream>>>(tab, reinterpret_cast<const double4*>(X), Tobs, n,
                                                                     p, j, dcand, partial);
-        k_fit_reduce<<<1, 32, 0, ctx->stream>>>(partial, (int)nb, n, dloss);
+        k_fit_reduce<<<1, 256, 0, ctx->stream>>>(partial, (int)nb, n, dloss);
         ctx->stats.kernel_launches += 2;
         cudaMemcpyAsync(losses.data(), dloss, 32 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
         return cudaStreamSynchronize(ctx->stream);
