@@ -276,9 +276,12 @@ __device__ __forceinline__ double unit_tf(const TupleConst& tc, const UnitState&
     return tf;
 }
 
-// B and B' of one block; returns T(B), writes T(B') - T(B)
+// B and B' of one block; returns T(B), writes T(B') - T(B).
+// Not inlined: it runs once per run and block, and one shared copy instead of four
+// inlined ones shrinks the eval loop's instruction footprint (same-box A/B: cfg2
+// 77.5 -> 74.5 ms, profiles/r1/ab_ni_summary.txt).
 template <bool UNIT>
-__device__ __forceinline__ double block_backward(const BlockConst& b, bool r1, double FH, double kG, double kA,
+__device__ __noinline__ double block_backward(const BlockConst& b, bool r1, double FH, double kG, double kA,
                                                  const FGRow* FG, double& dBp) {
     const double sAh = r1 ? b.sAh1 : b.sAh;
     const double CB = r1 ? b.C_B1 : b.C_B;                   // a checkpointed layer recomputes (L17)

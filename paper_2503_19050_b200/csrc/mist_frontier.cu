@@ -10,6 +10,9 @@
 //   pre = min y over elements before the last run head, cur = argmin (y, idx)
 //   from the last run head on; group heads reset the state.
 #include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -241,6 +244,152 @@ k_radix_scatter(const u64* __restrict__ t_in, const u32* __restrict__ g_in,
         const u32 gp = s_goff[d] + (u32)o - s_dstart[d];
         t_out[gp] = t; g_out[gp] = g; v_out[gp] = sk_v[o];
     }
+}
+
+// Persistent variant of k_radix_scatter with TMA bulk loads (sm_100a): each CTA
+// walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...; while it ranks and writes
+// tile i, the TMA engine already streams tile i+1 (t, g, v: three contiguous
+// cp.async.bulk copies completing on an mbarrier) into the other smem stage, and
+// the tile's 256 bucket offsets are prefetched one tile ahead.  Same ranking and
+// output as k_radix_scatter.  A partial last tile is loaded with plain loads.
+struct ScatterStage {
+    u64 t[kSortTile];
+    u32 g[kSortTile], v[kSortTile];
+};
+
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+    return (u32)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+    const u32 a = smem_u32(bar);
+    asm volatile("{\n .reg .pred P;\n WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+                 " @!P bra WAIT_%=;\n}\n" :: "r"(a), "r"(parity) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+k_radix_scatter_tma(const u64* __restrict__ t_in, const u32* __restrict__ g_in,
+                    const u32* __restrict__ v_in, u64* __restrict__ t_out,
+                    u32* __restrict__ g_out, u32* __restrict__ v_out, long long n, int pos,
+                    long long ntiles, const u32* __restrict__ block_off) {
+    constexpr int W = kThreads / 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    ScatterStage* stage = reinterpret_cast<ScatterStage*>(smem_raw);          // [2]
+    ScatterStage* sk = stage + 2;                                              // reordered tile
+    u32 (*s_cnt)[256] = reinterpret_cast<u32 (*)[256]>(sk + 1);                // [W][256]
+    u32* s_dstart = &s_cnt[W][0];
+    u32* s_goff = s_dstart + 256;
+    u32* s_wt = s_goff + 256;
+    u64* bar = reinterpret_cast<u64*>(s_wt + 32);                              // [2]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const long long full_tiles = n / kSortTile;
+    auto issue = [&](long long tile, int st) {   // thread 0: TMA the whole tile into stage st
+        const long long b = tile * kSortTile;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                     :: "r"(smem_u32(&bar[st])), "r"((u32)(kSortTile * 16)) : "memory");
+        bulk_g2s(stage[st].t, t_in + b, kSortTile * 8, &bar[st]);
+        bulk_g2s(stage[st].g, g_in + b, kSortTile * 4, &bar[st]);
+        bulk_g2s(stage[st].v, v_in + b, kSortTile * 4, &bar[st]);
+    };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    long long tile = blockIdx.x;
+    if (tid == 0 && tile < full_tiles) issue(tile, 0);
+    u32 goff_next = tile < ntiles ? block_off[(long long)tid * ntiles + tile] : 0u;
+    const u32 lt = (1u << lane) - 1;
+    for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it & 1;
+        const long long base = tile * kSortTile;
+        const long long next = tile + gridDim.x;
+        for (int i = 0; i < W; ++i) s_cnt[i][tid] = 0;
+        s_goff[tid] = goff_next;
+        if (next < ntiles) goff_next = block_off[(long long)tid * ntiles + next];   // one tile ahead
+        if (tid == 0 && next < full_tiles) {
+            // stage st^1 was last read before the previous iteration's closing barrier
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(next, st ^ 1);
+        }
+        const bool full = tile < full_tiles;
+        if (full) {
+            mbar_wait(&bar[st], (u32)(it >> 1) & 1u);   // the (it/2)-th use of stage st
+        } else {   // partial last tile: plain loads into the stage
+            for (int o = tid; o < kSortTile; o += kThreads) {
+                const long long i = base + o;
+                if (i < n) { stage[st].t[o] = t_in[i]; stage[st].g[o] = g_in[i]; stage[st].v[o] = v_in[i]; }
+            }
+        }
+        __syncthreads();
+        const ScatterStage& S = stage[st];
+        const int wbase = w * 32 * kSortItems;
+        u64 tv[kSortItems];
+        u32 gv[kSortItems], vv[kSortItems], dg[kSortItems], rk[kSortItems];
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            const int o = wbase + j * 32 + lane;
+            const bool valid = base + o < n;
+            tv[j] = S.t[o]; gv[j] = S.g[o]; vv[j] = S.v[o];
+            dg[j] = valid ? digit_of(tv[j], gv[j], pos) : 0xffffffffu;
+            const u32 peers = __match_any_sync(0xffffffffu, dg[j]);
+            const u32 before = valid ? s_cnt[w][dg[j]] : 0u;
+            rk[j] = before + __popc(peers & lt);
+            __syncwarp();
+            if (valid && (peers & lt) == 0) s_cnt[w][dg[j]] = before + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        {
+            u32 run = 0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const u32 c = s_cnt[k][tid];
+                s_cnt[k][tid] = run;
+                run += c;
+            }
+            u32 total;
+            s_dstart[tid] = block_excl_sum(run, s_wt, total);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            if (dg[j] == 0xffffffffu) continue;
+            const u32 o = s_dstart[dg[j]] + s_cnt[w][dg[j]] + rk[j];
+            sk->t[o] = tv[j]; sk->g[o] = gv[j]; sk->v[o] = vv[j];
+        }
+        __syncthreads();
+        const int tile_n = (int)min((long long)kSortTile, n - base);
+        for (int o = tid; o < tile_n; o += kThreads) {
+            const u64 t = sk->t[o];
+            const u32 g = sk->g[o];
+            const u32 d = digit_of(t, g, pos);
+            const u32 gp = s_goff[d] + (u32)o - s_dstart[d];
+            t_out[gp] = t; g_out[gp] = g; v_out[gp] = sk->v[o];
+        }
+        __syncthreads();
+    }
+}
+
+static size_t scatter_tma_smem() {
+    return 3 * sizeof(ScatterStage) + (kThreads / 32 + 2) * 256 * sizeof(u32) + 32 * sizeof(u32) + 2 * sizeof(u64);
+}
+
+// MIST_SCATTER=plain selects k_radix_scatter (A/B knob); default: the TMA-pipelined kernel.
+static bool scatter_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MIST_SCATTER");
+        v = (e && !strcmp(e, "plain")) ? 0 : 1;
+    }
+    return v == 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -497,9 +646,27 @@ cudaError_t frontier_reduce(cudaStream_t st, CandBuf cand, long long n, SortScra
                                                          S.block_hist);
         err = scan_u32_exclusive(st, S.block_hist, S.block_hist, 256 * ntiles, scan_tmp + 8, nullptr);
         if (err != cudaSuccess) return err;
-        k_radix_scatter<<<(unsigned)ntiles, T, 0, st>>>(S.key_t[cur], S.key_g[cur], S.val[cur],
-                                                         S.key_t[cur ^ 1], S.key_g[cur ^ 1],
-                                                         S.val[cur ^ 1], n, pos, ntiles, S.block_hist);
+        const bool aligned = ((reinterpret_cast<uintptr_t>(S.key_t[cur]) | reinterpret_cast<uintptr_t>(S.key_g[cur]) |
+                               reinterpret_cast<uintptr_t>(S.val[cur])) & 15) == 0;
+        if (scatter_tma() && aligned) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_radix_scatter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)scatter_tma_smem());
+                attr = true;
+            }
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            long long grid = std::min<long long>(ntiles, 2LL * sms);
+            k_radix_scatter_tma<<<(unsigned)grid, T, scatter_tma_smem(), st>>>(
+                S.key_t[cur], S.key_g[cur], S.val[cur], S.key_t[cur ^ 1], S.key_g[cur ^ 1], S.val[cur ^ 1], n, pos,
+                ntiles, S.block_hist);
+        } else {
+            k_radix_scatter<<<(unsigned)ntiles, T, 0, st>>>(S.key_t[cur], S.key_g[cur], S.val[cur],
+                                                             S.key_t[cur ^ 1], S.key_g[cur ^ 1],
+                                                             S.val[cur ^ 1], n, pos, ntiles, S.block_hist);
+        }
         rs->launches += 5;
         rs->passes++;
         cur ^= 1;
