@@ -749,7 +749,11 @@ k_eval(DevProblem P, EvalArgs A) {
 // runs of its 32 units round-robin to its lanes (owner found by binary lifting
 // over the warp prefix sum, unit state fetched with shuffles), so no lane idles
 // on an infeasible run while another works.
-template <bool UNIT, int NT, int MINB>
+// CQ = true: the queue spans the whole CTA instead of one warp -- the feasible runs
+// of all NT units are numbered by a block-wide prefix sum and warps take batches
+// of 32 from a shared-memory counter, so every warp of the CTA finishes the
+// window at about the same time (less time waiting at the window barrier).
+template <bool UNIT, int NT, int MINB, bool CQ>
 __global__ void __launch_bounds__(NT, MINB)
 k_eval_q(DevProblem P, EvalArgs A) {
     extern __shared__ double smem[];
@@ -757,6 +761,10 @@ k_eval_q(DevProblem P, EvalArgs A) {
     TupleConst* sT = reinterpret_cast<TupleConst*>(smem + 128);
     // per-unit forward state of the CTA's NT units (read by whichever lane runs a run of the unit)
     UnitState* sU = reinterpret_cast<UnitState*>(sT + ((NT + A.upt - 1) / A.upt + 1));
+    unsigned* s_incl = reinterpret_cast<unsigned*>(sU + NT);     // CQ: inclusive run-count prefix per unit
+    unsigned* s_g0 = s_incl + NT;                                 // CQ: first run (kG) per unit
+    unsigned* s_wt = s_g0 + NT;                                   // CQ: warp totals [NT/32]
+    unsigned* s_ctr = s_wt + NT / 32;                             // CQ: batch counter
     const int tid = threadIdx.x;
     load_fg(P, FG, tid);
     const double Q = P.Q;
@@ -815,27 +823,71 @@ k_eval_q(DevProblem P, EvalArgs A) {
             const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
             if ((int)lane >= o) incl += v;
         }
-        const unsigned excl = incl - cnt;
-        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned excl = incl - cnt;
+        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        if (CQ) {   // block-wide numbering of the runs
+            if (lane == 31) s_wt[tid >> 5] = incl;
+            if (tid == 0) *s_ctr = 0u;
+            __syncthreads();
+            unsigned before = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) {
+                const unsigned x = s_wt[w];
+                before += w < (tid >> 5) ? x : 0u;
+                all += x;
+            }
+            incl += before;
+            excl += before;
+            total = all;
+            s_incl[tid] = incl;
+            s_g0[tid] = g0;
+            __syncthreads();
+        }
         bool cv = false;                        // cached candidate (any group; emitted on group change)
         double ct = 0.0, cy = 0.0, cm = 0.0;
         u64 ci = 0;
         unsigned cgrp = 0;
-        for (unsigned rb = 0; rb < total; rb += 32) {
-            const unsigned r = rb + lane;
-            unsigned own = 0;                   // largest lane whose excl <= r
-#pragma unroll
-            for (int s2 = 16; s2 > 0; s2 >>= 1) {
-                const unsigned cand = own + s2;
-                const unsigned e = __shfl_sync(0xffffffffu, excl, cand & 31);
-                if (cand < 32 && e <= r) own = cand;
+        for (unsigned rb = 0;; rb += 32) {
+            if (CQ) {
+                unsigned b = 0;
+                if (lane == 0) b = atomicAdd(s_ctr, 32u);
+                rb = __shfl_sync(0xffffffffu, b, 0);
             }
-            const unsigned o_tk = __shfl_sync(0xffffffffu, tk, own);
-            const unsigned o_kW = __shfl_sync(0xffffffffu, kW, own);
-            const unsigned o_kA = __shfl_sync(0xffffffffu, kA, own);
-            const unsigned o_g0 = __shfl_sync(0xffffffffu, g0, own);
-            const unsigned o_ex = __shfl_sync(0xffffffffu, excl, own);
-            const UnitState& ou = wU[own];
+            if (rb >= total) break;
+            const unsigned r = rb + lane;
+            unsigned o_tk, o_kW, o_kA, o_g0, o_ex;
+            const UnitState* oup;
+            if (CQ) {
+                unsigned lo = 0, hi = NT - 1;       // first unit whose inclusive count exceeds r
+                while (lo < hi) {
+                    const unsigned mid = (lo + hi) >> 1;
+                    if (s_incl[mid] > r) hi = mid; else lo = mid + 1;
+                }
+                const unsigned own = lo;
+                o_ex = own ? s_incl[own - 1] : 0u;
+                o_g0 = s_g0[own];
+                const u64 uo = base + own;
+                o_tk = (unsigned)(uo / upt - tb0);
+                const unsigned jo = (unsigned)(uo - (tb0 + o_tk) * (u64)upt);
+                o_kW = jo / radix;
+                o_kA = jo - o_kW * radix;
+                oup = sU + own;
+            } else {
+                unsigned own = 0;                   // largest lane whose excl <= r
+#pragma unroll
+                for (int s2 = 16; s2 > 0; s2 >>= 1) {
+                    const unsigned cand = own + s2;
+                    const unsigned e = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && e <= r) own = cand;
+                }
+                o_tk = __shfl_sync(0xffffffffu, tk, own);
+                o_kW = __shfl_sync(0xffffffffu, kW, own);
+                o_kA = __shfl_sync(0xffffffffu, kA, own);
+                o_g0 = __shfl_sync(0xffffffffu, g0, own);
+                o_ex = __shfl_sync(0xffffffffu, excl, own);
+                oup = wU + own;
+            }
+            const UnitState& ou = *oup;
             bool emit = false;
             double et = 0.0, ey = 0.0, em = 0.0;
             u64 ei = 0;
@@ -977,7 +1029,7 @@ static int eval_cfg() {
     static int v = -1;
     if (v < 0) {
         const char* s = getenv("MIST_EVAL_CFG");
-        v = 1;   // default 256x3: measured best on cfg2 (profiles/r1, bench_r1i)
+        v = 0;   // default 256x2 (128 registers, no spills): best with the CTA queue (profiles/r1/ab_cq_summary.txt)
         if (s) {
             const char* names[5] = {"256x2", "256x3", "128x4", "128x5", "128x6"};
             for (int i = 0; i < 5; ++i)
@@ -987,43 +1039,50 @@ static int eval_cfg() {
     return v;
 }
 
-template <bool UNIT, int NT, int MINB>
+template <bool UNIT, int NT, int MINB, bool CQ>
 static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     static_assert(NT == kEvalThreads, "eval_smem_bytes sizes the tuple region for kEvalThreads");
-    const size_t smem = eval_smem_bytes(A.upt) + NT * sizeof(UnitState);
+    const size_t smem = eval_smem_bytes(A.upt) + NT * sizeof(UnitState) + (2 * NT + NT / 32 + 1) * sizeof(unsigned);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ>, NT, smem);
     if (per_sm < 1) per_sm = 1;
     u64 blocks = (A.n_units + NT - 1) / NT;
     const u64 cap = (u64)sm_count(device) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) return cudaSuccess;
-    k_eval_q<UNIT, NT, MINB><<<(unsigned)blocks, NT, smem, st>>>(P, A);
+    k_eval_q<UNIT, NT, MINB, CQ><<<(unsigned)blocks, NT, smem, st>>>(P, A);
     return cudaGetLastError();
 }
 
-// MIST_EVAL_QUEUE=0 selects the lockstep kG loop instead of the warp run queue.
-static bool eval_queue() {
+// MIST_EVAL_QUEUE=0 selects the lockstep kG loop, 1 the warp run queue, 2 (default)
+// the CTA-wide run queue.
+static int eval_queue() {
     static int v = -1;
     if (v < 0) {
         const char* s = getenv("MIST_EVAL_QUEUE");
-        v = (s && s[0] == '0') ? 0 : 1;
+        v = (s && s[0] == '0') ? 0 : (s && s[0] == '1') ? 1 : 2;
     }
-    return v == 1;
+    return v;
 }
 
 template <bool UNIT>
 static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
-    if (eval_queue()) {
+    if (eval_queue() == 2) {
         switch (eval_cfg()) {
-            case 0: return launch_eval_q<UNIT, 256, 2>(st, device, P, A);
-            default: return launch_eval_q<UNIT, 256, 3>(st, device, P, A);
+            case 0: return launch_eval_q<UNIT, 256, 2, true>(st, device, P, A);
+            default: return launch_eval_q<UNIT, 256, 3, true>(st, device, P, A);
+        }
+    }
+    if (eval_queue() == 1) {
+        switch (eval_cfg()) {
+            case 0: return launch_eval_q<UNIT, 256, 2, false>(st, device, P, A);
+            default: return launch_eval_q<UNIT, 256, 3, false>(st, device, P, A);
         }
     }
     switch (eval_cfg()) {
