@@ -756,15 +756,21 @@ k_eval(DevProblem P, EvalArgs A) {
 template <bool UNIT, int NT, int MINB, bool CQ>
 __global__ void __launch_bounds__(NT, MINB)
 k_eval_q(DevProblem P, EvalArgs A) {
-    extern __shared__ double smem[];
+    static_assert(sizeof(TupleConst) % 16 == 0, "bulk copies move whole tuples in 16-byte units");
+    extern __shared__ __align__(128) double smem[];
     FGRow* FG = reinterpret_cast<FGRow*>(smem);
-    TupleConst* sT = reinterpret_cast<TupleConst*>(smem + 128);
+    const int maxt = (NT + (int)A.upt - 1) / (int)A.upt + 1;        // tuples one window touches
+    TupleConst* sTbuf = reinterpret_cast<TupleConst*>(smem + 128);  // CQ: two stages of maxt tuples
+    TupleConst* sT = sTbuf;
     // per-unit forward state of the CTA's NT units (read by whichever lane runs a run of the unit)
-    UnitState* sU = reinterpret_cast<UnitState*>(sT + ((NT + A.upt - 1) / A.upt + 1));
-    unsigned* s_incl = reinterpret_cast<unsigned*>(sU + NT);     // CQ: inclusive run-count prefix per unit
-    unsigned* s_g0 = s_incl + NT;                                 // CQ: first run (kG) per unit
-    unsigned* s_wt = s_g0 + NT;                                   // CQ: warp totals [NT/32]
+    UnitState* sU = reinterpret_cast<UnitState*>(sTbuf + (CQ ? 2 : 1) * maxt);
+    unsigned* s_excl = reinterpret_cast<unsigned*>(sU + NT);     // CQ: exclusive run-count prefix per unit
+    unsigned* s_g0 = s_excl + NT;                                 // CQ: first run (kG) per unit
+    unsigned* s_uinfo = s_g0 + NT;                                // CQ: tk | kW << 10 | kA << 21
+    unsigned* s_wt = s_uinfo + NT;                                // CQ: warp totals [NT/32]
     unsigned* s_ctr = s_wt + NT / 32;                             // CQ: batch counter
+    u64* s_bar = reinterpret_cast<u64*>(s_ctr + 2);               // CQ: tuple-stage mbarriers [2]
+    unsigned short* s_map = reinterpret_cast<unsigned short*>(s_bar + 2);   // CQ: run -> unit [NT * Q1]
     const int tid = threadIdx.x;
     load_fg(P, FG, tid);
     const double Q = P.Q;
@@ -776,18 +782,56 @@ k_eval_q(DevProblem P, EvalArgs A) {
     const u64 n_units = A.n_units;
     unsigned nph = 0;
     unsigned ctr[4] = {0u, 0u, 0u, 0u};
-    for (u64 base = (u64)blockIdx.x * NT; base < n_units; base += (u64)gridDim.x * NT) {
-        const u64 last_unit = min(base + NT, n_units) - 1;
-        const u64 tb0 = base / upt, tb1 = last_unit / upt;
-        const int ntl = (int)(tb1 - tb0 + 1);
+    // CQ: the window's tuples arrive by one TMA bulk copy, issued one window ahead
+    auto tuples_of = [&](u64 b, u64& t0, int& nt) {
+        const u64 lu = min(b + NT, n_units) - 1;
+        t0 = b / upt;
+        nt = (int)(lu / upt - t0 + 1);
+    };
+    auto issue_tuples = [&](u64 b, int stg) {
+        u64 t0;
+        int nt;
+        tuples_of(b, t0, nt);
+        const unsigned bytes = (unsigned)(nt * sizeof(TupleConst));
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar[stg]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     :: "r"((unsigned)__cvta_generic_to_shared(sTbuf + stg * maxt)), "l"(A.tuples + t0), "r"(bytes),
+                        "r"(bar) : "memory");
+    };
+    if (CQ) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"((unsigned)__cvta_generic_to_shared(&s_bar[0])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"((unsigned)__cvta_generic_to_shared(&s_bar[1])) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            if ((u64)blockIdx.x * NT < n_units) issue_tuples((u64)blockIdx.x * NT, 0);
+        }
+    }
+    int it = 0;
+    for (u64 base = (u64)blockIdx.x * NT; base < n_units; base += (u64)gridDim.x * NT, ++it) {
+        u64 tb0;
+        int ntl;
+        tuples_of(base, tb0, ntl);
         __syncthreads();
-        {
+        if (CQ) {
+            const int stg = it & 1;
+            sT = sTbuf + stg * maxt;
+            const u64 nb = base + (u64)gridDim.x * NT;
+            if (tid == 0 && nb < n_units) {          // the other stage was last read before this barrier
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                issue_tuples(nb, stg ^ 1);
+            }
+            const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar[stg]);
+            const unsigned par = (unsigned)(it >> 1) & 1u;
+            asm volatile("{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+                         " @!P bra WAIT_%=;\n}\n" :: "r"(bar), "r"(par) : "memory");
+        } else {
             const double* src = reinterpret_cast<const double*>(A.tuples + tb0);
             double* dst = reinterpret_cast<double*>(sT);
             const int nw = ntl * (int)(sizeof(TupleConst) / 8);
             for (int i = tid; i < nw; i += NT) dst[i] = __ldg(src + i);
+            __syncthreads();
         }
-        __syncthreads();
         FiltView fv;
         fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
         const u64 u = base + tid;
@@ -839,8 +883,10 @@ k_eval_q(DevProblem P, EvalArgs A) {
             incl += before;
             excl += before;
             total = all;
-            s_incl[tid] = incl;
+            s_excl[tid] = excl;
             s_g0[tid] = g0;
+            s_uinfo[tid] = tk | (kW << 10) | (kA << 21);
+            for (unsigned k = excl; k < incl; ++k) s_map[k] = (unsigned short)tid;   // run -> unit
             __syncthreads();
         }
         bool cv = false;                        // cached candidate (any group; emitted on group change)
@@ -858,19 +904,13 @@ k_eval_q(DevProblem P, EvalArgs A) {
             unsigned o_tk, o_kW, o_kA, o_g0, o_ex;
             const UnitState* oup;
             if (CQ) {
-                unsigned lo = 0, hi = NT - 1;       // first unit whose inclusive count exceeds r
-                while (lo < hi) {
-                    const unsigned mid = (lo + hi) >> 1;
-                    if (s_incl[mid] > r) hi = mid; else lo = mid + 1;
-                }
-                const unsigned own = lo;
-                o_ex = own ? s_incl[own - 1] : 0u;
+                const unsigned own = r < total ? s_map[r] : 0u;
+                o_ex = s_excl[own];
                 o_g0 = s_g0[own];
-                const u64 uo = base + own;
-                o_tk = (unsigned)(uo / upt - tb0);
-                const unsigned jo = (unsigned)(uo - (tb0 + o_tk) * (u64)upt);
-                o_kW = jo / radix;
-                o_kA = jo - o_kW * radix;
+                const unsigned ui = s_uinfo[own];
+                o_tk = ui & 1023u;
+                o_kW = (ui >> 10) & 2047u;
+                o_kA = ui >> 21;
                 oup = sU + own;
             } else {
                 unsigned own = 0;                   // largest lane whose excl <= r
@@ -1042,7 +1082,10 @@ static int eval_cfg() {
 template <bool UNIT, int NT, int MINB, bool CQ>
 static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     static_assert(NT == kEvalThreads, "eval_smem_bytes sizes the tuple region for kEvalThreads");
-    const size_t smem = eval_smem_bytes(A.upt) + NT * sizeof(UnitState) + (2 * NT + NT / 32 + 1) * sizeof(unsigned);
+    const size_t maxt = (NT + A.upt - 1) / A.upt + 1;
+    const size_t smem = eval_smem_bytes(A.upt) + (CQ ? maxt * sizeof(TupleConst) : 0) + NT * sizeof(UnitState) +
+                        (3 * NT + NT / 32 + 2) * sizeof(unsigned) + 2 * sizeof(u64) +
+                        (CQ ? (size_t)NT * P.Q1 * sizeof(unsigned short) : 0);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {
