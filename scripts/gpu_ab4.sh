@@ -8,8 +8,8 @@ run() { # name lib cfg
   for st in 0.4 0.8 0.98; do MIST_LIB=$2 MIST_EVAL_CFG=$3 timeout 300 python tools/prof_step.py --workload 5 --start $st --fraction 0.01 --warmup 1 --steps 1 > gpurun_out/ab_${TAG}_$1_w${st}_1.log 2>&1; done
 }
 run base ab/libmist_base.so 256x2
-run pc ab/libmist_pc.so 256x2
-run tree ab/libmist_tree.so 256x2
-run tree128x5 ab/libmist_tree.so 128x5
+
+run wf ab/libmist_wf.so 256x2
+
 python scripts/ab_summ.py $TAG > gpurun_out/ab_${TAG}_summary.txt 2>&1
 echo done
