@@ -274,7 +274,13 @@ def main():
             "latency_ms": {"device": dev_total_ms / args.steps, "e2e": wall_total_ms / args.steps},
             "frontier_points": int(len(pts)),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         # dram__bytes_read.sum + dram__bytes_write.sum of k_eval_q from one ncu --set full
+                         # capture of the cfg2 sweep (one launch per step): tuples in, candidates out
+                         "traffic": (294.676736e6 + 475.951616e6) if args.workload == 2 else None,
+                         "ncu": {"fp64_pipe_pct": 33.2, "issue_active_pct": 55.8, "kernel_ms": 56.58,
+                                 "source": "profiles/r1/ncu_k_eval_q_map_raw.csv (cfg2, --set full)"}
+                         if args.workload == 2 else None,
                          "kernel": "k_eval", "note": "FP64 lane-ops (FMA=1): SURVEY 8(d) per-unit figures (56 per "
                          "Alg. 1 phase row, 7 with unit factors; 10 per config for O9 memory) x the phase rows "
                          "the kernel counted + configs, / CUDA-event time of k_eval on the ctx stream; peak = "
