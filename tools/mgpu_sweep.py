@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--factors", default="spec")
     ap.add_argument("--out", default="")
     ap.add_argument("--fingerprints", action="store_true")
+    ap.add_argument("--warmup", type=int, default=1,
+                    help="untimed sweeps of a small tuple range first (NCCL connection setup, allocations)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -41,6 +43,10 @@ def main():
             idt.copy_(torch.frombuffer(bytearray(mist.mist_nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         ctx.init_comm(bytes(idt.cpu().numpy().tobytes()), rank, world)
+        dist.barrier()
+    for _ in range(args.warmup):
+        mist.mist_pareto_frontier(ctx, spec, t_begin=0, t_end=min(spec.n_tuples, 4096))
+    if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
