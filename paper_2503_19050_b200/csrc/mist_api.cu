@@ -672,7 +672,14 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
             if (*p == ',') ++p;
         }
     } else {
-        levels.push_back(Q < 8 ? 2 : Q < 16 ? 3 : Q < 40 ? 5 : 7);
+        // measured (profiles/r1/ab_pl2_summary.txt): one level of 2 / 3 / 5 values up to Q < 40;
+        // for the Q = 50 space two levels {5, 11} (cfg5 windows -22% in sum vs one 7-value level)
+        if (Q < 40) {
+            levels.push_back(Q < 8 ? 2 : Q < 16 ? 3 : 5);
+        } else {
+            levels.push_back(5);
+            levels.push_back(11);
+        }
     }
     for (auto& nv : levels) nv = std::min(nv, Q + 1);
     const char* env = getenv("MIST_PILOT");

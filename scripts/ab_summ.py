@@ -3,7 +3,7 @@ import glob, json, re, sys, collections
 tag = sys.argv[1]
 rows = collections.defaultdict(list)
 for f in sorted(glob.glob(f"gpurun_out/ab_{tag}_*.log")):
-    m = re.match(rf"gpurun_out/ab_{tag}_(.+)_(cfg2|w[0-9.]+)_(\d)\.log", f)
+    m = re.match(rf"gpurun_out/ab_{tag}_(.+)_(cfg2|c[345]|w[0-9.]+)_(\d)\.log", f)
     if not m:
         continue
     lines = [l for l in open(f) if l.startswith("{")]
