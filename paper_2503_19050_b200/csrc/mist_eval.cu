@@ -6,11 +6,15 @@
 // (lines 476-492) with the interference model of Alg. 1 (lines 563-605);
 // memory per Eq. 4's constraint (line 683).  Readings O4-O9 in DESIGN.md.
 //
-// Thread mapping: one thread per OO-run = (tuple, kW, kG, kA); it loops over
-// kO = 0..Q.  t never reads OO (P13), so the stable phases (F, B, B' of every
-// block) are evaluated once per run and only the first-microbatch forward F'
-// and the memory are evaluated per config.  Memory is evaluated as exact
-// integers scaled by D = Q*TP*DP (O9), so feasibility is bit-exact.
+// Work decomposition: unit = (tuple, kW, kA) -> OO-run = unit + kG -> config =
+// run + kO.  t never reads OO (P13), so the F phases are evaluated once per unit,
+// B and B' once per run, and only the first-microbatch forward F' and the memory
+// per config.  Memory is evaluated as exact integers scaled by D = Q*TP*DP (O9),
+// so feasibility is bit-exact.  The frontier sweep (k_eval_q, CTA run queue):
+// each CTA takes a window of 256 units, one per thread for the per-unit setup;
+// the feasible runs of the window are numbered by a block prefix sum and dealt
+// to warps in batches of 32 from a shared counter.  k_eval is the
+// lockstep variant used for the dense outputs and the pilot sub-grid sweeps.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>

@@ -7,5 +7,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench_${TAG}_default.log 2>&1
 timeout 600 python bench.py --factors unit --no-cpu-baseline > gpurun_out/bench_${TAG}_unit.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg2_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1
-bash scripts/gpu_prof_eval.sh $TAG
+MIST_FULLSCALE=1 timeout 1500 python -m pytest tests/test_gpu_fullscale.py -q -m gpu -k "5" --timeout=1400 -p no:cacheprovider > gpurun_out/pytest_fullscale_cfg5_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_fullscale_cfg5_$TAG.log
 echo done
