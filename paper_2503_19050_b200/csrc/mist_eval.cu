@@ -967,19 +967,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
             }
             warp_emit(emit, et, ey, em, ei, egrp, A, lane);
         }
-        // window flush: drop a cached candidate that another lane's candidate of the same
-        // group beats (a real feasible config, so it is not on the frontier, O10)
-        bool keep = cv;
-#pragma unroll 1
-        for (int sft = 1; sft < 32; ++sft) {
-            const int src = (lane + sft) & 31;
-            const bool ov = __shfl_sync(0xffffffffu, cv, src);
-            const unsigned og = __shfl_sync(0xffffffffu, cgrp, src);
-            const double ot = __shfl_sync(0xffffffffu, ct, src), oy = __shfl_sync(0xffffffffu, cy, src);
-            const u64 oi = __shfl_sync(0xffffffffu, ci, src);
-            if (keep && ov && og == cgrp && beats(ot, oy, oi, ct, cy, ci)) keep = false;
-        }
-        warp_emit(keep, ct, cy, cm, ci, cgrp, A, lane);
+        warp_emit(cv, ct, cy, cm, ci, cgrp, A, lane);
     }
     if (A.phases) {
         unsigned v = nph;
