@@ -757,21 +757,25 @@ k_eval(DevProblem P, EvalArgs A) {
 // of all NT units are numbered by a block-wide prefix sum and warps take batches
 // of 32 from a shared-memory counter, so every warp of the CTA finishes the
 // window at about the same time (less time waiting at the window barrier).
-template <bool UNIT, int NT, int MINB, bool CQ>
+// UPW (CTA queue only): units per thread per window; a window of NT*UPW units
+// halves the window boundaries (and their barrier tails) for UPW = 2.
+template <bool UNIT, int NT, int MINB, bool CQ, int UPW>
 __global__ void __launch_bounds__(NT, MINB)
 k_eval_q(DevProblem P, EvalArgs A) {
+    static_assert(CQ || UPW == 1, "several units per thread need the CTA queue");
+    constexpr int NW = NT * UPW;                                     // units per window
     static_assert(sizeof(TupleConst) % 16 == 0, "bulk copies move whole tuples in 16-byte units");
     extern __shared__ __align__(128) double smem[];
     FGRow* FG = reinterpret_cast<FGRow*>(smem);
-    const int maxt = (NT + (int)A.upt - 1) / (int)A.upt + 1;        // tuples one window touches
+    const int maxt = (NW + (int)A.upt - 1) / (int)A.upt + 1;        // tuples one window touches
     TupleConst* sTbuf = reinterpret_cast<TupleConst*>(smem + 128);  // CQ: two stages of maxt tuples
     TupleConst* sT = sTbuf;
     // per-unit forward state of the CTA's NT units (read by whichever lane runs a run of the unit)
     UnitState* sU = reinterpret_cast<UnitState*>(sTbuf + (CQ ? 2 : 1) * maxt);
-    unsigned* s_excl = reinterpret_cast<unsigned*>(sU + NT);     // CQ: exclusive run-count prefix per unit
-    unsigned* s_g0 = s_excl + NT;                                 // CQ: first run (kG) per unit
-    unsigned* s_uinfo = s_g0 + NT;                                // CQ: tk | kW << 10 | kA << 21
-    unsigned* s_wt = s_uinfo + NT;                                // CQ: warp totals [NT/32]
+    unsigned* s_excl = reinterpret_cast<unsigned*>(sU + NW);     // CQ: exclusive run-count prefix per unit
+    unsigned* s_g0 = s_excl + NW;                                 // CQ: first run (kG) per unit
+    unsigned* s_uinfo = s_g0 + NW;                                // CQ: tk | kW << 10 | kA << 21
+    unsigned* s_wt = s_uinfo + NW;                                // CQ: warp totals [NT/32]
     unsigned* s_ctr = s_wt + NT / 32;                             // CQ: batch counter
     u64* s_bar = reinterpret_cast<u64*>(s_ctr + 2);               // CQ: tuple-stage mbarriers [2]
     unsigned short* s_map = reinterpret_cast<unsigned short*>(s_bar + 2);   // CQ: run -> unit [NT * Q1]
@@ -788,7 +792,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
     unsigned ctr[4] = {0u, 0u, 0u, 0u};
     // CQ: the window's tuples arrive by one TMA bulk copy, issued one window ahead
     auto tuples_of = [&](u64 b, u64& t0, int& nt) {
-        const u64 lu = min(b + NT, n_units) - 1;
+        const u64 lu = min(b + NW, n_units) - 1;
         t0 = b / upt;
         nt = (int)(lu / upt - t0 + 1);
     };
@@ -808,11 +812,11 @@ k_eval_q(DevProblem P, EvalArgs A) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"((unsigned)__cvta_generic_to_shared(&s_bar[0])) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"((unsigned)__cvta_generic_to_shared(&s_bar[1])) : "memory");
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-            if ((u64)blockIdx.x * NT < n_units) issue_tuples((u64)blockIdx.x * NT, 0);
+            if ((u64)blockIdx.x * NW < n_units) issue_tuples((u64)blockIdx.x * NW, 0);
         }
     }
     int it = 0;
-    for (u64 base = (u64)blockIdx.x * NT; base < n_units; base += (u64)gridDim.x * NT, ++it) {
+    for (u64 base = (u64)blockIdx.x * NW; base < n_units; base += (u64)gridDim.x * NW, ++it) {
         u64 tb0;
         int ntl;
         tuples_of(base, tb0, ntl);
@@ -820,7 +824,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
         if (CQ) {
             const int stg = it & 1;
             sT = sTbuf + stg * maxt;
-            const u64 nb = base + (u64)gridDim.x * NT;
+            const u64 nb = base + (u64)gridDim.x * NW;
             if (tid == 0 && nb < n_units) {          // the other stage was last read before this barrier
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 issue_tuples(nb, stg ^ 1);
@@ -838,61 +842,71 @@ k_eval_q(DevProblem P, EvalArgs A) {
         }
         FiltView fv;
         fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
-        const u64 u = base + tid;
-        const unsigned tk = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
-        const unsigned jj = (unsigned)(u - (tb0 + tk) * (u64)upt);
-        const unsigned kW = jj / radix, kA = jj - kW * radix;
-        const bool active = u < n_units && jj < radix * radix && kW <= (unsigned)P.kmax[0] &&
-                            kA <= (unsigned)P.kmax[3];                   // preset ranges
-        const unsigned gend = (unsigned)P.kmax[1] + 1u;                  // runs kG < gend
-        unsigned g0 = radix;
-        {
-            const TupleConst& tc = sT[tk];
-            if (active) {
-                UnitState us;
-                unit_forward<UNIT>(tc, (double)kW, (double)kA, FG, us);
-                wU[lane] = us;
-                nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
-                       (unsigned)(tc.last != 0);
-                RunState rm;
-                const double kOend = (double)P.kmax[2];
-                for (unsigned ig = 0; ig < gend; ++ig) {
-                    run_memory(tc, (double)kW, (double)ig, (double)kA, Q, rm);
-                    if (mem_kO(tc, rm, kOend, Q) <= tc.DMB) { g0 = ig; break; }
+        unsigned total = 0;
+        // per-thread state of unit j = 0 (the warp queue of the non-CQ path reads it)
+        unsigned tk = 0, kW = 0, kA = 0, g0 = radix, excl = 0;
+#pragma unroll
+        for (int j = 0; j < UPW; ++j) {
+            const unsigned w = (unsigned)(j * NT + tid);                   // unit of the window
+            const u64 u = base + w;
+            const unsigned tkj = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
+            const unsigned jj = (unsigned)(u - (tb0 + tkj) * (u64)upt);
+            const unsigned kWj = jj / radix, kAj = jj - kWj * radix;
+            const bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
+                                kAj <= (unsigned)P.kmax[3];              // preset ranges
+            const unsigned gend = (unsigned)P.kmax[1] + 1u;              // runs kG < gend
+            unsigned g0j = radix;
+            {
+                const TupleConst& tc = sT[tkj];
+                if (active) {
+                    UnitState us;
+                    unit_forward<UNIT>(tc, (double)kWj, (double)kAj, FG, us);
+                    sU[w] = us;
+                    nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
+                           (unsigned)(tc.last != 0);
+                    RunState rm;
+                    const double kOend = (double)P.kmax[2];
+                    for (unsigned ig = 0; ig < gend; ++ig) {
+                        run_memory(tc, (double)kWj, (double)ig, (double)kAj, Q, rm);
+                        if (mem_kO(tc, rm, kOend, Q) <= tc.DMB) { g0j = ig; break; }
+                    }
+                    if (!(tc.mG >= tc.gb_k)) g0j = 0;  // no kG-suffix property: every run is a task
                 }
-                if (!(tc.mG >= tc.gb_k)) g0 = 0;      // no kG-suffix property: every run is a task
             }
-        }
-        __syncwarp();
-        const unsigned cnt = (active && g0 < gend) ? gend - g0 : 0u;
-        unsigned incl = cnt;
+            __syncwarp();
+            const unsigned cnt = (active && g0j < gend) ? gend - g0j : 0u;
+            unsigned incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((int)lane >= o) incl += v;
-        }
-        unsigned excl = incl - cnt;
-        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-        if (CQ) {   // block-wide numbering of the runs
-            if (lane == 31) s_wt[tid >> 5] = incl;
-            if (tid == 0) *s_ctr = 0u;
-            __syncthreads();
-            unsigned before = 0, all = 0;
-#pragma unroll
-            for (int w = 0; w < NT / 32; ++w) {
-                const unsigned x = s_wt[w];
-                before += w < (tid >> 5) ? x : 0u;
-                all += x;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += v;
             }
-            incl += before;
-            excl += before;
-            total = all;
-            s_excl[tid] = excl;
-            s_g0[tid] = g0;
-            s_uinfo[tid] = tk | (kW << 10) | (kA << 21);
-            for (unsigned k = excl; k < incl; ++k) s_map[k] = (unsigned short)tid;   // run -> unit
-            __syncthreads();
+            unsigned exj = incl - cnt;
+            unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (CQ) {   // block-wide numbering of the runs, after the window's units of earlier j
+                if (j > 0) __syncthreads();              // s_wt of the previous j has been read
+                if (lane == 31) s_wt[tid >> 5] = incl;
+                if (tid == 0 && j == 0) *s_ctr = 0u;
+                __syncthreads();
+                unsigned before = 0, all = 0;
+#pragma unroll
+                for (int wq = 0; wq < NT / 32; ++wq) {
+                    const unsigned x = s_wt[wq];
+                    before += wq < (tid >> 5) ? x : 0u;
+                    all += x;
+                }
+                incl += total + before;
+                exj += total + before;
+                tot = total + all;
+                s_excl[w] = exj;
+                s_g0[w] = g0j;
+                s_uinfo[w] = tkj | (kWj << 10) | (kAj << 21);
+                for (unsigned k = exj; k < incl; ++k) s_map[k] = (unsigned short)w;   // run -> unit
+            }
+            total = tot;
+            if (j == 0) { tk = tkj; kW = kWj; kA = kAj; g0 = g0j; excl = exj; }
         }
+        if (CQ) __syncthreads();
         bool cv = false;                        // cached candidate (any group; emitted on group change)
         double ct = 0.0, cy = 0.0, cm = 0.0;
         u64 ci = 0;
@@ -1083,28 +1097,38 @@ static int eval_cfg() {
     return v;
 }
 
-template <bool UNIT, int NT, int MINB, bool CQ>
+template <bool UNIT, int NT, int MINB, bool CQ, int UPW = 1>
 static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
-    static_assert(NT == kEvalThreads, "eval_smem_bytes sizes the tuple region for kEvalThreads");
-    const size_t maxt = (NT + A.upt - 1) / A.upt + 1;
-    const size_t smem = eval_smem_bytes(A.upt) + (CQ ? maxt * sizeof(TupleConst) : 0) + NT * sizeof(UnitState) +
-                        (3 * NT + NT / 32 + 2) * sizeof(unsigned) + 2 * sizeof(u64) +
-                        (CQ ? (size_t)NT * P.Q1 * sizeof(unsigned short) : 0);
+    constexpr size_t NW = (size_t)NT * UPW;
+    const size_t maxt = (NW + A.upt - 1) / A.upt + 1;
+    const size_t smem = 128 * sizeof(double) + (CQ ? 2 : 1) * maxt * sizeof(TupleConst) + NW * sizeof(UnitState) +
+                        (3 * NW + NT / 32 + 2) * sizeof(unsigned) + 2 * sizeof(u64) +
+                        (CQ ? NW * P.Q1 * sizeof(unsigned short) : 0);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ, UPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW>, NT, smem);
     if (per_sm < 1) per_sm = 1;
-    u64 blocks = (A.n_units + NT - 1) / NT;
+    u64 blocks = (A.n_units + NW - 1) / NW;
     const u64 cap = (u64)sm_count(device) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) return cudaSuccess;
-    k_eval_q<UNIT, NT, MINB, CQ><<<(unsigned)blocks, NT, smem, st>>>(P, A);
+    k_eval_q<UNIT, NT, MINB, CQ, UPW><<<(unsigned)blocks, NT, smem, st>>>(P, A);
     return cudaGetLastError();
+}
+
+// MIST_EVAL_UPW=2: windows of 512 units (2 per thread) for the CTA queue (A/B knob).
+static int eval_upw() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("MIST_EVAL_UPW");
+        v = (s && s[0] == '2') ? 2 : 1;
+    }
+    return v;
 }
 
 // MIST_EVAL_QUEUE=0 selects the lockstep kG loop, 1 the warp run queue, 2 (default)
@@ -1121,6 +1145,7 @@ static int eval_queue() {
 template <bool UNIT>
 static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     if (eval_queue() == 2) {
+        if (eval_upw() == 2) return launch_eval_q<UNIT, 256, 2, true, 2>(st, device, P, A);
         switch (eval_cfg()) {
             case 0: return launch_eval_q<UNIT, 256, 2, true>(st, device, P, A);
             default: return launch_eval_q<UNIT, 256, 3, true>(st, device, P, A);
