@@ -1121,12 +1121,13 @@ static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& 
     return cudaGetLastError();
 }
 
-// MIST_EVAL_UPW=2: windows of 512 units (2 per thread) for the CTA queue (A/B knob).
+// Units per thread per window of the CTA queue: 2 by default (windows of 512 units;
+// cfg2 62.5 -> 60.2 ms, profiles/r1/ab_upw_summary.txt); MIST_EVAL_UPW=1 for 256.
 static int eval_upw() {
     static int v = -1;
     if (v < 0) {
         const char* s = getenv("MIST_EVAL_UPW");
-        v = (s && s[0] == '2') ? 2 : 1;
+        v = (s && s[0] == '1') ? 1 : 2;
     }
     return v;
 }
