@@ -277,9 +277,9 @@ def main():
                          "frac": achieved / peak,
                          # dram__bytes_read.sum + dram__bytes_write.sum of k_eval_q from one ncu --set full
                          # capture of the cfg2 sweep (one launch per step): tuples in, candidates out
-                         "traffic": (294.676736e6 + 475.951616e6) if args.workload == 2 else None,
-                         "ncu": {"fp64_pipe_pct": 33.2, "issue_active_pct": 55.8, "kernel_ms": 56.58,
-                                 "source": "profiles/r1/ncu_k_eval_q_map_raw.csv (cfg2, --set full)"}
+                         "traffic": (291.711232e6 + 457.023232e6) if args.workload == 2 else None,
+                         "ncu": {"fp64_pipe_pct": 33.9, "issue_active_pct": 56.3, "kernel_ms": 54.54,
+                                 "source": "profiles/r1/ncu_k_eval_q_final_raw.csv (cfg2, --set full)"}
                          if args.workload == 2 else None,
                          "kernel": "k_eval", "note": "FP64 lane-ops (FMA=1): SURVEY 8(d) per-unit figures (56 per "
                          "Alg. 1 phase row, 7 with unit factors; 10 per config for O9 memory) x the phase rows "
