@@ -330,14 +330,14 @@ def mist_pareto_frontier(ctx: Context, spec: Spec, t_begin: int = 0, t_end: int 
     fph = np.zeros(ng, dtype=np.uint64) if fingerprints else None
     if out is None:
         cap = max(1024, 64 * ng)
-        pts = np.zeros(cap, dtype=POINT_DTYPE)
+        pts = np.empty(cap, dtype=POINT_DTYPE)     # written by the library up to n_out
     else:
         pts = out
         cap = len(out) if isinstance(out, np.ndarray) else out.numel() // 4
     st = L.mist_pareto_frontier(ctx.handle, *spec.args(), t_begin, t_end, ykey, _ptr(pts), cap, C.byref(n),
                                 _ptr(offs), _ptr(fpc), _ptr(fph))
     if st == 3 and out is None:
-        pts = np.zeros(n.value, dtype=POINT_DTYPE)
+        pts = np.empty(n.value, dtype=POINT_DTYPE)
         st = L.mist_pareto_frontier(ctx.handle, *spec.args(), t_begin, t_end, ykey, _ptr(pts), n.value,
                                     C.byref(n), _ptr(offs), _ptr(fpc), _ptr(fph))
     ctx.check(st, "mist_pareto_frontier")
