@@ -34,6 +34,8 @@ int coef_row(const mist_coeffs_t*, int, int);
 // from mist_eval.cu
 cudaError_t launch_precompute(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                               u64, u64, TupleConst*);
+cudaError_t launch_precompute_segs(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
+                                   const u64*, int, u64, TupleConst*);
 cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, int);
 size_t eval_smem_bytes(unsigned upt);
 unsigned units_per_tuple(unsigned radix);
@@ -345,7 +347,7 @@ extern "C" void mist_ctx_destroy(mist_ctx_t* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
     for (DevBuf* b : {&ctx->cand_mem, &ctx->sort_mem, &ctx->tuples, &ctx->scan_tmp, &ctx->groups,
-                      &ctx->coef, &ctx->counters, &ctx->fp, &ctx->xfer, &ctx->out, &ctx->foff})
+                      &ctx->coef, &ctx->counters, &ctx->fp, &ctx->xfer, &ctx->out, &ctx->foff, &ctx->segs})
         release(*b);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -687,12 +689,29 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     for (const auto& ch : chunks) {
         u64 nT = 0;
         int h = ev_begin(ctx, CAT_PRE);
-        for (const auto& seg : ch) {
+        if (ch.size() == 1) {
+            const auto& seg = ch[0];
             CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, seg.first,
-                                 seg.second - seg.first, (TupleConst*)ctx->tuples.p + nT), "precompute");
-            nT += seg.second - seg.first;
-            ctx->stats.kernel_launches += 1;
+                                 seg.second - seg.first, (TupleConst*)ctx->tuples.p), "precompute");
+            nT = seg.second - seg.first;
+        } else {
+            // a block-cyclic share: every segment in one launch (segment table uploaded once)
+            std::vector<u64> tab(2 * ch.size() + 2);
+            for (size_t k = 0; k < ch.size(); ++k) {
+                tab[2 * k] = ch[k].first;
+                tab[2 * k + 1] = nT;
+                nT += ch[k].second - ch[k].first;
+            }
+            tab[2 * ch.size()] = 0;
+            tab[2 * ch.size() + 1] = nT;
+            CK(ensure(ctx->segs, sizeof(u64) * tab.size()), "alloc segs");
+            CK(cudaMemcpyAsync(ctx->segs.p, tab.data(), sizeof(u64) * tab.size(), cudaMemcpyHostToDevice,
+                               ctx->stream), "upload segs");
+            CK(launch_precompute_segs(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef,
+                                      (const u64*)ctx->segs.p, (int)ch.size(), nT, (TupleConst*)ctx->tuples.p),
+               "precompute");
         }
+        ctx->stats.kernel_launches += 1;
         ev_end(ctx, h);
         const TupleConst* tup = (const TupleConst*)ctx->tuples.p;
         if (pilot) {

@@ -140,6 +140,24 @@ __device__ void make_tuple(const DevProblem& P, const DevGroup* groups, int ng,
     if (P.ckpt_ends && c != 0 && c != l) o.DMB = -1.0;
 }
 
+// a2 over a rank's block-cyclic share: seg[2*s] = first tuple of segment s,
+// seg[2*s+1] = its first position in `out` (prefix of the segment lengths,
+// seg[2*nseg+1] = total); one launch for all segments.
+__global__ void k_tuple_precompute_segs(DevProblem P, const DevGroup* __restrict__ groups, int ng,
+                                        const double* __restrict__ coef, const u64* __restrict__ seg, int nseg,
+                                        u64 nT, TupleConst* __restrict__ out) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nT; i += (u64)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nseg - 1;                  // last segment whose first position <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (seg[2 * mid + 1] <= i) lo = mid; else hi = mid - 1;
+        }
+        TupleConst tc;
+        make_tuple(P, groups, ng, coef, seg[2 * lo] + (i - seg[2 * lo + 1]), tc);
+        out[i] = tc;
+    }
+}
+
 __global__ void k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ groups, int ng,
                                    const double* __restrict__ coef, u64 T0, u64 nT,
                                    TupleConst* __restrict__ out) {
@@ -1046,6 +1064,17 @@ cudaError_t launch_precompute(cudaStream_t st, int device, const DevProblem& P, 
     const u64 cap = (u64)sm_count(device) * 16;
     if (blocks > cap) blocks = cap;
     k_tuple_precompute<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, T0, nT, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_precompute_segs(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,
+                                   int ng, const double* coef, const u64* seg, int nseg, u64 nT, TupleConst* out) {
+    if (nT == 0) return cudaSuccess;
+    const int threads = 128;
+    u64 blocks = (nT + threads - 1) / threads;
+    const u64 cap = (u64)sm_count(device) * 16;
+    if (blocks > cap) blocks = cap;
+    k_tuple_precompute_segs<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, seg, nseg, nT, out);
     return cudaGetLastError();
 }
 
