@@ -15,6 +15,6 @@ while [ $n -le $N ]; do
   echo "rc=$?" >> gpurun_out/bench_${TAG}_n$n.log
   n=$((n*2))
 done
-timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29512 tools/mgpu_sweep.py --workload 5 > gpurun_out/cfg5_${TAG}_n$N.log 2>&1
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29512 tools/mgpu_sweep.py --workload 5 --plan > gpurun_out/cfg5_${TAG}_n$N.log 2>&1
 echo "rc=$?" >> gpurun_out/cfg5_${TAG}_n$N.log
 echo done

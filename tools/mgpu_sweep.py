@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--factors", default="spec")
     ap.add_argument("--out", default="")
     ap.add_argument("--fingerprints", action="store_true")
+    ap.add_argument("--plan", action="store_true", help="rank 0 also solves the inter-stage plan (Eq. 2-3)")
     ap.add_argument("--warmup", type=int, default=1,
                     help="untimed sweeps of a small tuple range first (NCCL connection setup, allocations)")
     args = ap.parse_args()
@@ -70,6 +71,13 @@ def main():
                "device_s_per_rank": [round(float(x[1]) / 1e3, 3) for x in per_rank]}
         if args.fingerprints:
             out["feasible_configs"] = int(fc.sum())
+        if args.plan:
+            pb = workload(args.workload, factors=args.factors)
+            ts = time.perf_counter()
+            plan = mist.mist_solve_inter(spec.groups, pts, offs, pb.model.L, pb.N * pb.M)
+            out["plan"] = {"solve_s": time.perf_counter() - ts, "G": plan["G"], "S": plan["S"],
+                           "objective_s": plan["objective"], "labels": int(plan["labels"]),
+                           "sweep_to_plan_s": float(w[0]) + time.perf_counter() - ts}
         print(json.dumps(out), flush=True)
         if args.out:
             np.savez_compressed(args.out, points=pts, offsets=offs, fp_count=fc, fp_hash=fh)
