@@ -71,14 +71,16 @@ def main():
                "device_s_per_rank": [round(float(x[1]) / 1e3, 3) for x in per_rank]}
         if args.fingerprints:
             out["feasible_configs"] = int(fc.sum())
+        print(json.dumps(out), flush=True)
         if args.plan:
             pb = workload(args.workload, factors=args.factors)
             ts = time.perf_counter()
             plan = mist.mist_solve_inter(spec.groups, pts, offs, pb.model.L, pb.N * pb.M)
-            out["plan"] = {"solve_s": time.perf_counter() - ts, "G": plan["G"], "S": plan["S"],
-                           "objective_s": plan["objective"], "labels": int(plan["labels"]),
-                           "sweep_to_plan_s": float(w[0]) + time.perf_counter() - ts}
-        print(json.dumps(out), flush=True)
+            el = time.perf_counter() - ts
+            print(json.dumps({"plan": {"solve_s": el, "G": plan["G"], "S": plan["S"],
+                                       "objective_s": plan["objective"], "labels": int(plan["labels"]),
+                                       "sweep_to_plan_s": float(w[0]) + el,
+                                       "host_threads": os.cpu_count()}}), flush=True)
         if args.out:
             np.savez_compressed(args.out, points=pts, offsets=offs, fp_count=fc, fp_hash=fh)
     ctx.close()
