@@ -243,20 +243,51 @@ extern "C" mist_status_t mist_solve_inter(const mist_group_t* groups, int64_t n_
                 seed = std::min(seed, v);
             }
         }
+    unsigned nt = n_threads > 0 ? (unsigned)n_threads : std::max(1u, std::thread::hardware_concurrency());
+    nt = std::min<unsigned>(nt, (unsigned)Gs.size());
+    auto run_all = [&](const Problem& q, double inc, std::vector<Result>& res) {
+        res.assign(Gs.size(), Result());
+        std::atomic<size_t> next{0};
+        auto worker = [&]() {
+            for (size_t i; (i = next.fetch_add(1)) < Gs.size();) res[i] = solve_G(q, Gs[i], inc);
+        };
+        std::vector<std::thread> th;
+        for (unsigned i = 1; i < nt; ++i) th.emplace_back(worker);
+        worker();
+        for (auto& t : th) t.join();
+    };
+    // A tighter incumbent from a thinned candidate set (at most 4 points per group: the
+    // ends and two inner points of each frontier): its optimum is a real plan, so the
+    // exact DP may prune every label whose bound reaches it.  Pruning with a valid upper
+    // bound explores the same plans below it, so the result is unchanged.
+    const int64_t n_pts = group_offsets[n_groups];
+    if (n_pts > 8 * n_groups) {
+        std::vector<mist_point_t> tp;
+        std::vector<int64_t> to(n_groups + 1, 0);
+        tp.reserve((size_t)n_groups * 4);
+        for (int64_t g = 0; g < n_groups; ++g) {
+            const int64_t a = group_offsets[g], n = group_offsets[g + 1] - a;
+            if (n <= 4) {
+                for (int64_t k = 0; k < n; ++k) tp.push_back(points[a + k]);
+            } else {
+                const int64_t pick[4] = {0, n / 3, (2 * n) / 3, n - 1};
+                for (int64_t k : pick) tp.push_back(points[a + k]);
+            }
+            to[g + 1] = (int64_t)tp.size();
+        }
+        Problem thin = pb;
+        thin.pts = tp.data();
+        thin.offs = to.data();
+        std::vector<Result> rt;
+        run_all(thin, std::nextafter(seed, std::numeric_limits<double>::infinity()), rt);
+        for (const Result& r : rt)
+            if (r.S > 0) seed = std::min(seed, r.val);
+    }
     // the seed only prunes; a plan equal to it is found again by its own G's DP
     const double inc = std::nextafter(seed, std::numeric_limits<double>::infinity());
 
-    std::vector<Result> res(Gs.size());
-    unsigned nt = n_threads > 0 ? (unsigned)n_threads : std::max(1u, std::thread::hardware_concurrency());
-    nt = std::min<unsigned>(nt, (unsigned)Gs.size());
-    std::atomic<size_t> next{0};
-    auto worker = [&]() {
-        for (size_t i; (i = next.fetch_add(1)) < Gs.size();) res[i] = solve_G(pb, Gs[i], inc);
-    };
-    std::vector<std::thread> th;
-    for (unsigned i = 1; i < nt; ++i) th.emplace_back(worker);
-    worker();
-    for (auto& t : th) t.join();
+    std::vector<Result> res;
+    run_all(pb, inc, res);
 
     int best = -1;
     int64_t labels = 0;

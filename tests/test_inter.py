@@ -198,3 +198,18 @@ def test_solver_real_frontier_cfg_tiny():
     arr, offs = _csr(thin)
     plan = mist.mist_solve_inter(mist.group_array(keys), arr, offs, 4, 4)
     _check_plan(plan, keys, thin, 4, 4, want)
+
+
+def test_solver_many_points_per_group():
+    # > 8 candidates per group: the solver first solves a thinned table for its incumbent
+    # (mist_inter.cpp); the optimum must still equal the exhaustive argmin
+    pb = tiny(3, 4, 1, 2, 4, 2)
+    keys = _tiny_keys(pb)
+    for rep in range(2):
+        pts = random_candidates(keys, seed=700 + rep, max_points=12, p_empty=0.0)
+        pts = [p + [(t + 40.0, max(0.0, d - 5.0)) for t, d in p] for p in pts]     # 2..24 points
+        assert sum(len(p) for p in pts) > 8 * len(keys)
+        want, _ = inter.brute_force_plan({k: p for k, p in zip(keys, pts)}, L=3, devices=2)
+        arr, offs = _csr(pts)
+        plan = mist.mist_solve_inter(mist.group_array(keys), arr, offs, 3, 2)
+        _check_plan(plan, keys, pts, 3, 2, want)
