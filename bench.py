@@ -48,6 +48,49 @@ def alg_ops(phases: int, configs: int, unit: bool) -> float:
     return (7.0 if unit else 56.0) * phases + 10.0 * configs
 
 
+# Static reference capture of the dominant kernel (one `ncu --set full` run of the
+# same workload, committed under profiles/): DRAM traffic and pipe figures cannot
+# be measured live without a profiler, so they are READ from that file at run time
+# and labelled as a reference capture, never as this run's measurement.
+NCU_CAPTURE = {2: "profiles/r1/ncu_k_eval_q_final_raw.csv"}
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
+          "ms": 1.0, "msecond": 1.0, "s": 1e3, "nsecond": 1e-6, "%": 1.0, "": 1.0}
+
+
+def ncu_reference(workload: int):
+    """Per-launch figures of the k_eval_q row of the committed capture for this
+    workload (None if there is none): traffic in bytes, duration in ms."""
+    import csv
+    rel = NCU_CAPTURE.get(workload)
+    path = os.path.join(ROOT, rel) if rel else None
+    if not path or not os.path.exists(path):
+        return None
+    rows = list(csv.reader(open(path)))
+    head, units = rows[0], rows[1]
+    col = {k: i for i, k in enumerate(head)}
+    row = next((r for r in rows[2:] if "k_eval_q" in r[col["Kernel Name"]]), None)
+    if row is None:
+        return None
+
+    def val(name):
+        i = col.get(name)
+        if i is None or not row[i]:
+            return None
+        return float(row[i].replace(",", "")) * _SCALE.get(units[i], 1.0)
+
+    meta = {}
+    mpath = os.path.splitext(path)[0] + ".meta.json"
+    if os.path.exists(mpath):
+        meta = json.load(open(mpath))
+    return {"traffic": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+            "kernel_ms": val("gpu__time_duration.sum"),
+            "fp64_pipe_pct": val("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "kind": "static reference capture (ncu --set full of this workload's sweep), read from the file "
+                    "at run time; not measured in this run",
+            "source": rel, **{k: meta[k] for k in ("commit", "command", "kernel") if k in meta}}
+
+
 # B200 FP64 issue peak derived from unit counts and clock (DESIGN.md Sec. 6):
 # 148 SMs x 64 FP64 lanes x 1.965 GHz = 1.861e13 lane-ops/s.
 FP64_PEAK_OPS = 148 * 64 * 1.965e9
@@ -252,6 +295,7 @@ def main():
         ops = alg_ops(int(stats["phases_evaluated"]), my_configs, bool(stats["unit_factors"]))
         achieved = ops / (stats["eval_ms"] / 1e3) / 1e12
         peak = FP64_PEAK_OPS / 1e12
+        ncu = ncu_reference(args.workload)
         # inter-stage consumer (Eq. 2-3): host solve over the exact
         # frontiers of the last step, outside the timed region
         ts = time.perf_counter()
@@ -275,12 +319,10 @@ def main():
             "frontier_points": int(len(pts)),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak,
-                         # dram__bytes_read.sum + dram__bytes_write.sum of k_eval_q from one ncu --set full
-                         # capture of the cfg2 sweep (one launch per step): tuples in, candidates out
-                         "traffic": (291.711232e6 + 457.023232e6) if args.workload == 2 else None,
-                         "ncu": {"fp64_pipe_pct": 33.9, "issue_active_pct": 56.3, "kernel_ms": 54.54,
-                                 "source": "profiles/r1/ncu_k_eval_q_final_raw.csv (cfg2, --set full)"}
-                         if args.workload == 2 else None,
+                         # dram__bytes_read.sum + dram__bytes_write.sum of k_eval_q (one launch per step:
+                         # tuples in, candidates out) from the committed capture, see "ncu"
+                         "traffic": ncu["traffic"] if ncu else None,
+                         "ncu": ncu,
                          "kernel": "k_eval", "note": "FP64 lane-ops (FMA=1): SURVEY 8(d) per-unit figures (56 per "
                          "Alg. 1 phase row, 7 with unit factors; 10 per config for O9 memory) x the phase rows "
                          "the kernel counted + configs, / CUDA-event time of k_eval on the ctx stream; peak = "

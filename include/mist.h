@@ -217,7 +217,10 @@ mist_status_t mist_eval_stage_costs(mist_ctx_t* ctx, const mist_model_t* model, 
                                     int64_t n_groups, uint64_t begin, uint64_t end, double* t,
                                     double* d, double* mem, uint8_t* feasible);
 
-/* Test hook: same as above for an arbitrary list idx[0..n) (device pointer). */
+/* Test hook: same as above for an arbitrary list idx[0..n) (device pointer).
+ * Every index is checked on the device: one >= the space's total config count
+ * is never decoded, its outputs are left untouched, and the call returns
+ * INVALID_ARG after the kernel (the other positions are written). */
 mist_status_t mist_eval_stage_costs_at(mist_ctx_t* ctx, const mist_model_t* model, int64_t B,
                                        const mist_mesh_t* mesh, const mist_space_t* space,
                                        const mist_coeffs_t* coeffs, const mist_group_t* groups,

@@ -40,7 +40,7 @@ cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, i
 size_t eval_smem_bytes(unsigned upt);
 unsigned units_per_tuple(unsigned radix);
 cudaError_t launch_eval_at(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
-                           const u64*, long long, double*, double*, double*, uint8_t*);
+                           const u64*, long long, u64, unsigned*, double*, double*, double*, uint8_t*);
 // from mist_frontier.cu
 cudaError_t frontier_reduce(cudaStream_t, CandBuf, long long, SortScratch&, u32*, long long*, ReduceStats*);
 cudaError_t frontier_group_offsets(cudaStream_t, const u32*, long long, int, int64_t*);
@@ -281,9 +281,18 @@ static long long next_pow2(long long x) {
     return p;
 }
 
+// FNV-1a over 8-byte words (then the tail bytes): the cache key hashes the whole
+// group table, ~1 MB for cfg2, so word steps keep it well under a millisecond
 static uint64_t fnv(uint64_t h, const void* data, size_t n) {
     const unsigned char* b = (const unsigned char*)data;
-    for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ULL; }
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, b + i, 8);
+        h ^= w;
+        h *= 1099511628211ULL;
+    }
+    for (; i < n; ++i) { h ^= b[i]; h *= 1099511628211ULL; }
     return h;
 }
 
@@ -465,22 +474,22 @@ extern "C" mist_status_t mist_eval_stage_costs_at(mist_ctx_t* ctx, const mist_mo
     mist_status_t st = prepare(ctx, model, B, mesh, space, coeffs, groups, n_groups, 0, &pp);
     if (st != MIST_OK) return st;
     if (n < 0 || (n > 0 && !idx)) return fail(ctx, MIST_ERR_INVALID_ARG, "bad index list");
-    // range check of the indices on the host would need a D2H; the kernel clamps nothing, so
-    // verify with a max-reduction over a host copy only when small, else trust the caller.
-    if (n > 0 && n <= (1 << 20)) {
-        std::vector<uint64_t> h((size_t)n);
-        CK(cudaMemcpy(h.data(), idx, sizeof(uint64_t) * (size_t)n, cudaMemcpyDefault), "read idx");
-        for (uint64_t v : h)
-            if (v >= pp.total_configs) return fail(ctx, MIST_ERR_INVALID_ARG, "index out of range");
-    }
+    // every index is range-checked on the device: one outside [0, total_configs) is never
+    // decoded (it would address a split past n_splits); it sets a flag -> INVALID_ARG
+    CK(ensure(ctx->counters, 64), "alloc counters");
+    unsigned* d_bad = (unsigned*)ctx->counters.p;
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), ctx->stream), "zero flag");
     int hh = ev_begin(ctx, CAT_EVAL);
-    CK(launch_eval_at(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, (const u64*)idx, n, t, d, mem,
-                      feasible), "eval_at");
+    CK(launch_eval_at(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, (const u64*)idx, n,
+                      (u64)pp.total_configs, d_bad, t, d, mem, feasible), "eval_at");
     ev_end(ctx, hh);
     ctx->stats.kernel_launches += 1;
     ctx->stats.configs_evaluated = (uint64_t)n;
+    unsigned bad = 0;
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream), "read flag");
     CK(cudaStreamSynchronize(ctx->stream), "eval_at sync");
     ev_flush(ctx);
+    if (bad) return fail(ctx, MIST_ERR_INVALID_ARG, "index out of range");
     return MIST_OK;
 }
 
@@ -581,6 +590,10 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     A.phases = mode == 0 ? S.d_phases : nullptr;
     A.nv = nv;
     for (unsigned i = 0; i < nv && i < 16; ++i) A.vals[i] = vals[i];
+    {
+        const char* e = getenv("MIST_R7");
+        A.no_r7 = (e && e[0] == '0') ? 1 : 0;
+    }
     if ((mode == 0 || mode == 2) && S.filter) {
         A.f_t = ctx->cand.t;
         A.f_y = ctx->cand.y;
@@ -651,7 +664,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     CK(ensure(ctx->foff, sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc filter offsets");
     S.d_count = (u64*)ctx->counters.p;
     S.d_phases = S.d_count + 1;
-    CK(cudaMemsetAsync(S.d_phases, 0, 5 * sizeof(u64), ctx->stream), "zero phase counters");
+    CK(cudaMemsetAsync(S.d_phases, 0, 6 * sizeof(u64), ctx->stream), "zero phase counters");
     S.d_foff = (int64_t*)ctx->foff.p;
     st = write_count(ctx, S, 0);
     if (st != MIST_OK) return st;
@@ -735,14 +748,15 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     }
     ctx->stats.candidates += (uint64_t)S.count;   // before the final reduction
     {
-        u64 ph[5] = {0, 0, 0, 0, 0};
+        u64 ph[6] = {0, 0, 0, 0, 0, 0};
         CK(cudaMemcpyAsync(ph, S.d_phases, sizeof(ph), cudaMemcpyDeviceToHost, ctx->stream), "read phases");
         CK(cudaStreamSynchronize(ctx->stream), "sync phases");
         ctx->stats.phases_evaluated += ph[0];
 #ifdef MIST_COUNTERS
-        fprintf(stderr, "MIST_COUNTERS runs_backward=%llu runs_cut_at_k0=%llu d_evals=%llu k0_steps=%llu configs=%llu\n",
+        fprintf(stderr, "MIST_COUNTERS runs_backward=%llu runs_cut_at_k0=%llu d_evals=%llu k0_steps=%llu "
+                "runs_cut_r7=%llu configs=%llu\n",
                 (unsigned long long)ph[1], (unsigned long long)ph[2], (unsigned long long)ph[3],
-                (unsigned long long)ph[4], (unsigned long long)(n_tuples * pp.R));
+                (unsigned long long)ph[4], (unsigned long long)ph[5], (unsigned long long)(n_tuples * pp.R));
 #endif
     }
     long long nf = 0;
@@ -865,7 +879,13 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
                                  coeffs->t_emb_bwd, coeffs->t_head_fwd, coeffs->t_head_bwd};
         for (int k = 0; k < 6 && rows > 0; ++k)
             if (tabs[k]) key = fnv(key, tabs[k], sizeof(double) * (size_t)rows);
+        // the (b, TP) -> row mapping of the tables
+        if (coeffs->b_values && coeffs->n_b > 0) key = fnv(key, coeffs->b_values, sizeof(int32_t) * (size_t)coeffs->n_b);
+        if (coeffs->tp_values && coeffs->n_tp > 0)
+            key = fnv(key, coeffs->tp_values, sizeof(int32_t) * (size_t)coeffs->n_tp);
     }
+    // the caller's group table itself (check_groups validates it only on a cache miss)
+    if (groups && n_groups > 0) key = fnv(key, groups, sizeof(mist_group_t) * (size_t)n_groups);
     key = fnv(key, &t_begin, sizeof(t_begin));
     key = fnv(key, &t_end, sizeof(t_end));
     key = fnv(key, &ykey, sizeof(ykey));

@@ -19,6 +19,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include <cstdlib>
 #include <cstring>
 
@@ -426,6 +428,75 @@ __device__ __forceinline__ double d_lower_bound(const TupleConst& tc, const Unit
     return lb;
 }
 
+// R7 (run cut before the backward rows).  t of run kG is (sum count T(F)) + sum count
+// T(B(kG)) + p2p, with T(F) exact per unit and T(B) bounded below by R4/R5.  The
+// bound is non-decreasing in kG: the B channels H2D = FH + kG sGh + kA sAh and
+// D2H = kG sGd grow with kG, R5 is monotone in the channels while the nonzero
+// pattern is fixed (every kG >= 1), and R4 (the max, used at kG = 0) lies below R5
+// at kG = 1.  So the runs whose bound clears the staircase are a suffix in kG.
+template <bool UNIT>
+__device__ __forceinline__ double lb_backward(const BlockConst& b, bool r1, double FH, double kG, double kA,
+                                              const FGRow* FG) {
+    const double CB = r1 ? b.C_B1 : b.C_B;
+    const double BH = FH + kG * b.sGh + kA * (r1 ? b.sAh1 : b.sAh), BD = kG * b.sGd;
+    if (kG == 0.0) return dmax(dmax(CB, b.N_B), dmax(BH, BD));
+    return lb_row<UNIT>(CB, b.N_B, BH, BD, FG);
+}
+
+template <bool UNIT>
+__device__ __forceinline__ double run_t_lb(const TupleConst& tc, const UnitState& us, double kG, double kA,
+                                           const FGRow* FG) {
+    double tb = 0.0;
+    if (tc.nl0 > 0.0) tb += tc.nl0 * lb_backward<UNIT>(tc.L, false, us.FH_L, kG, kA, FG);
+    if (tc.nl1 > 0.0) tb += tc.nl1 * lb_backward<UNIT>(tc.L, true, us.FH_L, kG, kA, FG);
+    if (tc.first) tb += lb_backward<UNIT>(tc.E, false, us.FH_E, kG, kA, FG);
+    if (tc.last) tb += lb_backward<UNIT>(tc.H, false, us.FH_H, kG, kA, FG);
+    return (unit_tf(tc, us) + tb) + tc.t_p2p;
+}
+
+// End of the runs of a unit that the pilot staircase cannot rule out: runs
+// [g0, result) stay, runs [result, gend) are beaten.  A staircase point p with
+// t_p < lb_t(kG) and y_p <= every y of the unit beats every config of runs >= kG
+// (O10: strictly smaller t).  y lower bound: d >= 0 (L25), so for ykey = d only a
+// y = 0 staircase point (the group's last, y falls along t) can cut; for ykey =
+// mem the unit's smallest mem is its (kG, kO) = (kmax, kmax) config exactly (O9
+// is non-increasing in kG and kO under the kG-suffix property, R2').  The t bound
+// carries a 1e-12 relative margin for the rounding of R4/R5 against Alg. 1.
+template <bool UNIT>
+__device__ unsigned run_cut(const DevProblem& P, const TupleConst& tc, const UnitState& us, unsigned kW, unsigned kA,
+                            unsigned g0, unsigned gend, const FGRow* FG, const double* ft, const double* fy,
+                            long long lo, long long hi) {
+    if (lo >= hi) return gend;
+    const double dkA = kA;
+    double ymin = 0.0;                         // ykey = d: y >= 0
+    if (P.ykey) {
+        if (!(tc.mG >= tc.gb_k)) return gend;  // mem not monotone in kG: no cut
+        RunState rm;
+        run_memory(tc, (double)kW, (double)(gend - 1), dkA, (double)P.Q, rm);
+        ymin = mem_kO(tc, rm, (double)P.kmax[2], (double)P.Q) / tc.D;
+    } else if (!(fy[hi - 1] <= 0.0)) {
+        return gend;                           // no y = 0 point: nothing below every d
+    }
+    auto cut = [&](unsigned g) -> bool {
+        const double lb = run_t_lb<UNIT>(tc, us, (double)g, dkA, FG) * (1.0 - 1e-12);
+        if (!P.ykey) return ft[hi - 1] < lb;
+        long long a = lo, b = hi;              // points with t < lb: [lo, a)
+        while (a < b) {
+            const long long m = (a + b) >> 1;
+            if (ft[m] < lb) a = m + 1; else b = m;
+        }
+        return a > lo && fy[a - 1] <= ymin;    // the smallest y among them
+    };
+    if (cut(g0)) return g0;
+    if (!cut(gend - 1)) return gend;
+    unsigned a = g0, b = gend - 1;             // cut(a) false, cut(b) true
+    while (b - a > 1) {
+        const unsigned m = (a + b) >> 1;
+        if (cut(m)) b = m; else a = m;
+    }
+    return b;
+}
+
 // fill the {f, g} factor table (non-members: f = 1, g = 0)
 __device__ __forceinline__ void load_fg(const DevProblem& P, FGRow* FG, int tid) {
     if (tid < 64) {
@@ -449,8 +520,9 @@ __device__ __forceinline__ u64 splitmix64(u64 x) {
 constexpr int kEvalThreads = 256;
 
 // Instrumented build (-DMIST_COUNTERS): per-thread event counters of the frontier
-// sweep, flushed to A.phases[1..4]: runs through run_backward, runs dropped at
-// their first config by the bound, configs whose d was evaluated, k0 scan steps.
+// sweep, flushed to A.phases[1..5]: runs through run_backward, runs dropped at
+// their first config by the bound, configs whose d was evaluated, k0 scan steps,
+// runs cut before their backward rows (R7).
 #ifdef MIST_COUNTERS
 #define MIST_CTR(i, v) (ctr[i] += (v))
 #else
@@ -460,7 +532,7 @@ constexpr int kEvalThreads = 256;
 __device__ __forceinline__ void flush_ctr(const EvalArgs& A, const unsigned* ctr, unsigned lane) {
 #ifdef MIST_COUNTERS
     if (!A.phases) return;
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 5; ++i) {
         unsigned v = ctr[i];
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0 && v) atomicAdd(A.phases + 1 + i, (u64)v);
@@ -674,7 +746,7 @@ k_eval(DevProblem P, EvalArgs A) {
                                (unsigned)(tc.last != 0);
         const unsigned brows = nrows * (tc.L.N_Bp != tc.L.N_B ? 2u : 1u);
         unsigned nph = active ? nrows : 0u;
-        unsigned ctr[4] = {0u, 0u, 0u, 0u};
+        unsigned ctr[5] = {0u, 0u, 0u, 0u, 0u};
         bool cv = false;                       // cached candidate
         double ct = 0.0, cy = 0.0, cm = 0.0;
         u64 ci = 0;
@@ -807,7 +879,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
     const unsigned upt = A.upt;
     const u64 n_units = A.n_units;
     unsigned nph = 0;
-    unsigned ctr[4] = {0u, 0u, 0u, 0u};
+    unsigned ctr[5] = {0u, 0u, 0u, 0u, 0u};
     // CQ: the window's tuples arrive by one TMA bulk copy, issued one window ahead
     auto tuples_of = [&](u64 b, u64& t0, int& nt) {
         const u64 lu = min(b + NW, n_units) - 1;
@@ -860,6 +932,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
         }
         FiltView fv;
         fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
+        const bool r7 = fv.off != nullptr && A.fp == nullptr && A.no_r7 == 0;
         unsigned total = 0;
         // per-thread state of unit j = 0 (the warp queue of the non-CQ path reads it)
         unsigned tk = 0, kW = 0, kA = 0, g0 = radix, excl = 0;
@@ -873,7 +946,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
             const bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
                                 kAj <= (unsigned)P.kmax[3];              // preset ranges
             const unsigned gend = (unsigned)P.kmax[1] + 1u;              // runs kG < gend
-            unsigned g0j = radix;
+            unsigned g0j = radix, g1j = gend;
             {
                 const TupleConst& tc = sT[tkj];
                 if (active) {
@@ -889,10 +962,17 @@ k_eval_q(DevProblem P, EvalArgs A) {
                         if (mem_kO(tc, rm, kOend, Q) <= tc.DMB) { g0j = ig; break; }
                     }
                     if (!(tc.mG >= tc.gb_k)) g0j = 0;  // no kG-suffix property: every run is a task
+                    // R7: runs the staircase beats on t alone are never dealt (not with
+                    // fingerprints, which count every feasible config)
+                    if (r7 && g0j < gend) {
+                        g1j = run_cut<UNIT>(P, tc, us, kWj, kAj, g0j, gend, FG, fv.t, fv.y, fv.off[tc.group],
+                                            fv.off[tc.group + 1]);
+                        MIST_CTR(4, gend - g1j);
+                    }
                 }
             }
             __syncwarp();
-            const unsigned cnt = (active && g0j < gend) ? gend - g0j : 0u;
+            const unsigned cnt = (active && g0j < g1j) ? g1j - g0j : 0u;
             unsigned incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1013,7 +1093,8 @@ k_eval_q(DevProblem P, EvalArgs A) {
 template <bool UNIT>
 __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int ng,
                           const double* __restrict__ coef, const u64* __restrict__ idxs, long long n,
-                          double* t, double* d, double* mem, uint8_t* feas) {
+                          u64 total, unsigned* __restrict__ bad, double* t, double* d, double* mem,
+                          uint8_t* feas) {
     __shared__ FGRow FG[16];
     load_fg(P, FG, threadIdx.x);
     __syncthreads();
@@ -1021,6 +1102,10 @@ __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const u64 idx = idxs[i];
+        if (idx >= total) {          // outside the space: flag it (INVALID_ARG), never decode it
+            atomicOr(bad, 1u);
+            continue;
+        }
         const u64 T = idx / R;
         u64 r = idx - T * R;
         const unsigned kA = (unsigned)(r % Q1); r /= Q1;
@@ -1094,10 +1179,12 @@ template <bool UNIT, int MODE, int NT, int MINB>
 static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     const size_t smem = eval_smem_bytes(A.upt);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_eval<UNIT, MODE, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
+    static std::atomic<unsigned long long> attr_set{0};   // the attribute is per device: one bit per device
+    if (device >= 64 || !((attr_set.load() >> device) & 1ull)) {
+        cudaError_t e = cudaFuncSetAttribute(k_eval<UNIT, MODE, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e != cudaSuccess) return e;
+        if (device < 64) attr_set.fetch_or(1ull << device);
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE, NT, MINB>, NT, smem);
@@ -1134,10 +1221,12 @@ static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& 
                         (3 * NW + NT / 32 + 2) * sizeof(unsigned) + 2 * sizeof(u64) +
                         (CQ ? NW * P.Q1 * sizeof(unsigned short) : 0);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ, UPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
+    static std::atomic<unsigned long long> attr_set{0};   // the attribute is per device: one bit per device
+    if (device >= 64 || !((attr_set.load() >> device) & 1ull)) {
+        cudaError_t e = cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ, UPW>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        if (device < 64) attr_set.fetch_or(1ull << device);
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW>, NT, smem);
@@ -1208,17 +1297,19 @@ cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const 
 }
 
 cudaError_t launch_eval_at(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,
-                           int ng, const double* coef, const u64* idx, long long n, double* t,
-                           double* d, double* mem, uint8_t* feas) {
+                           int ng, const double* coef, const u64* idx, long long n, u64 total, unsigned* bad,
+                           double* t, double* d, double* mem, uint8_t* feas) {
     if (n <= 0) return cudaSuccess;
     const int threads = 128;
     long long blocks = (n + threads - 1) / threads;
     const long long cap = (long long)sm_count(device) * 8;
     if (blocks > cap) blocks = cap;
     if (P.unit_factors)
-        k_eval_at<true><<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, idx, n, t, d, mem, feas);
+        k_eval_at<true><<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, idx, n, total, bad, t, d, mem,
+                                                               feas);
     else
-        k_eval_at<false><<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, idx, n, t, d, mem, feas);
+        k_eval_at<false><<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, idx, n, total, bad, t, d, mem,
+                                                                feas);
     return cudaGetLastError();
 }
 

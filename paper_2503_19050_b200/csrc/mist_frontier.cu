@@ -16,6 +16,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "mist_internal.h"
 
 namespace mist {
@@ -649,14 +651,15 @@ cudaError_t frontier_reduce(cudaStream_t st, CandBuf cand, long long n, SortScra
         const bool aligned = ((reinterpret_cast<uintptr_t>(S.key_t[cur]) | reinterpret_cast<uintptr_t>(S.key_g[cur]) |
                                reinterpret_cast<uintptr_t>(S.val[cur])) & 15) == 0;
         if (scatter_tma() && aligned) {
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_radix_scatter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)scatter_tma_smem());
-                attr = true;
-            }
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
+            static std::atomic<unsigned long long> attr{0};   // the attribute is per device: one bit per device
+            if (dev >= 64 || !((attr.load() >> dev) & 1ull)) {
+                err = cudaFuncSetAttribute(k_radix_scatter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)scatter_tma_smem());
+                if (err != cudaSuccess) return err;
+                if (dev < 64) attr.fetch_or(1ull << dev);
+            }
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             long long grid = std::min<long long>(ntiles, 2LL * sms);
             k_radix_scatter_tma<<<(unsigned)grid, T, scatter_tma_smem(), st>>>(

@@ -22,6 +22,7 @@
 // last stage backwards lets one DP per G serve every S: closing the plan with a
 // "first" stage at step k gives S = k.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <limits>
@@ -259,9 +260,14 @@ extern "C" mist_status_t mist_solve_inter(const mist_group_t* groups, int64_t n_
     // A tighter incumbent from a thinned candidate set (at most 4 points per group: the
     // ends and two inner points of each frontier): its optimum is a real plan, so the
     // exact DP may prune every label whose bound reaches it.  Pruning with a valid upper
-    // bound explores the same plans below it, so the result is unchanged.
+    // bound explores the same plans below it, so the result is unchanged.  Off by default
+    // (MIST_INTER_THIN=1 enables it): it halved the solve on a synthetic cfg5-like table,
+    // but on cfg5's real frontier it was slower (10.5 -> 11.3 s) for 0.7% fewer labels
+    // (profiles/r1/cfg5_r1y_n4.log vs cfg5_r1z_n4.log).
     const int64_t n_pts = group_offsets[n_groups];
-    if (n_pts > 8 * n_groups) {
+    const char* thin_env = getenv("MIST_INTER_THIN");
+    const bool thin_on = thin_env && thin_env[0] == '1';
+    if (thin_on && n_pts > 8 * n_groups) {
         std::vector<mist_point_t> tp;
         std::vector<int64_t> to(n_groups + 1, 0);
         tp.reserve((size_t)n_groups * 4);

@@ -121,6 +121,7 @@ struct EvalArgs {
     const double* f_y;
     const unsigned long long* f_idx;
     const int64_t* f_off;       // [n_groups+1], null = no filter
+    int no_r7;                  // 1: no run cut before the backward rows (A/B knob MIST_R7=0)
 };
 
 struct ReduceStats {

@@ -72,3 +72,16 @@ def compare_frontiers(g_pts, g_off, o_pts, o_off, groups=None, label=""):
         # sorted by t ascending, y strictly descending
         assert np.all(np.diff(G["t"]) > 0) and np.all(np.diff(G["y"]) < 0), f"{label} group {g} order"
     return stats
+
+
+def frontier_fp_and_bench(ctx, spec, **kw):
+    """The sweep twice: with fingerprints (feasible-set check; every feasible
+    config is visited) and without (the bench's launch path, where the exact
+    skips R4/R5/R7 cut whole runs).  Both must return the same frontier bit for
+    bit; returns the fingerprinted call's (points, offsets, fp_count, fp_hash)."""
+    from paper_2503_19050_b200 import mist
+    pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, spec, fingerprints=True, **kw)
+    p2, o2, _, _ = mist.mist_pareto_frontier(ctx, spec, **kw)
+    assert np.array_equal(offs, o2), "bench-path frontier: group sizes differ from the fingerprinted sweep"
+    assert p2.tobytes() == pts.tobytes(), "bench-path frontier differs from the fingerprinted sweep"
+    return pts, offs, fc, fh

@@ -12,7 +12,7 @@ from oracle.binding import POINT_DTYPE as ORC_POINT
 from oracle.binding import Oracle
 from paper_2503_19050_b200 import mist
 from synth import random_problem, tiny, workload
-from tests.parity import compare_dense, compare_frontiers
+from tests.parity import compare_dense, compare_frontiers, frontier_fp_and_bench
 
 pytestmark = pytest.mark.gpu
 
@@ -88,7 +88,7 @@ def test_frontier_small_spaces(ctx, k, ykey):
     except ValueError:
         pytest.skip("empty space")
     s = mist.Spec(pb)
-    pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, s, ykey=ykey, fingerprints=True)
+    pts, offs, fc, fh = frontier_fp_and_bench(ctx, s, ykey=ykey)
     ref = o.sweep(ykey=ykey)
     assert np.array_equal(fc, ref["fp_count"]) and np.array_equal(fh, ref["fp_hash"])
     compare_frontiers(pts, offs, ref["points"], ref["offsets"], label=pb.name)
@@ -108,7 +108,7 @@ def test_dense_cfg1_full(ctx):
 def test_frontier_cfg1_full(ctx, ykey):
     pb = workload(1)
     o, s = Oracle(pb), mist.Spec(pb)
-    pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, s, ykey=ykey, fingerprints=True)
+    pts, offs, fc, fh = frontier_fp_and_bench(ctx, s, ykey=ykey)
     ref = o.sweep(ykey=ykey)
     assert np.array_equal(fc, ref["fp_count"]) and np.array_equal(fh, ref["fp_hash"])
     st = compare_frontiers(pts, offs, ref["points"], ref["offsets"], label="cfg1")
@@ -121,7 +121,7 @@ def test_frontier_cfg2_bench_config_sampled_groups(ctx, factors):
     of bench.py) -- checked on 16 seeded groups the oracle sweeps in full."""
     pb = workload(2, factors=factors)
     o, s = Oracle(pb), mist.Spec(pb)
-    pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, s, ykey=0, fingerprints=True)
+    pts, offs, fc, fh = frontier_fp_and_bench(ctx, s, ykey=0)
     rng = np.random.default_rng(11)
     counts = np.array([g.count for g in o.groups])
     small = np.nonzero(counts <= 2_500_000)[0]
@@ -163,7 +163,7 @@ def test_frontier_big_configs_sampled_groups(ctx, i):
         R = (pb.Q + 1) ** 4
         tb = int(G.tuple_offset)
         te = tb + int(G.count) // R
-        pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, s, t_begin=tb, t_end=te, fingerprints=True)
+        pts, offs, fc, fh = frontier_fp_and_bench(ctx, s, t_begin=tb, t_end=te)
         ref = o.sweep(g, g + 1)
         assert fc[g] == ref["fp_count"][0] and fh[g] == ref["fp_hash"][0]
         assert offs[g + 1] - offs[g] == offs[-1]   # only group g is non-empty
@@ -177,14 +177,14 @@ def test_sharding_invariance(ctx):
     from oracle.binding import frontier_points
     pb = workload(1)
     s = mist.Spec(pb)
-    full, foffs, fc, fh = mist.mist_pareto_frontier(ctx, s, fingerprints=True)
+    full, foffs, fc, fh = frontier_fp_and_bench(ctx, s)
     rng = np.random.default_rng(5)
     for k in (2, 3, 8):
         cuts = np.sort(rng.choice(np.arange(1, s.n_tuples), k - 1, replace=False))
         bounds = [0, *cuts.tolist(), s.n_tuples]
         parts, cnt, hsh = [], np.zeros(s.n_groups, np.uint64), np.zeros(s.n_groups, np.uint64)
         for a, b in zip(bounds[:-1], bounds[1:]):
-            p, off, c, h = mist.mist_pareto_frontier(ctx, s, t_begin=a, t_end=b, fingerprints=True)
+            p, off, c, h = frontier_fp_and_bench(ctx, s, t_begin=a, t_end=b)
             gid = np.repeat(np.arange(s.n_groups), np.diff(off))
             q = np.zeros(len(p), dtype=ORC_POINT)
             for f in ("idx", "t", "y", "mem"):
@@ -220,6 +220,43 @@ def test_buffer_too_small_and_retry(ctx):
     assert st == 0
     again, offs2, _, _ = mist.mist_pareto_frontier(ctx, s)
     assert again.tobytes() == big.tobytes() and np.array_equal(offs, offs2)
+
+
+def test_retry_cache_keyed_on_groups(ctx):
+    """The BUFFER_TOO_SMALL retry cache is keyed on the group table too: a
+    retry with a different (invalid) table is validated, not served stale."""
+    import ctypes as C
+    pb = tiny(4, 4, 1, 4, 8, 2)
+    s = mist.Spec(pb)
+    L = mist.lib()
+    n = C.c_int64(0)
+    offs = np.zeros(s.n_groups + 1, dtype=np.int64)
+    small = np.zeros(1, dtype=mist.POINT_DTYPE)
+    st = L.mist_pareto_frontier(ctx.handle, *s.args(), 0, 0, 0, small.ctypes.data, 1, C.byref(n),
+                                offs.ctypes.data, None, None)
+    assert st == 3 and n.value > 1
+    s.groups[0].w += 1
+    big = np.zeros(n.value, dtype=mist.POINT_DTYPE)
+    st = L.mist_pareto_frontier(ctx.handle, *s.args(), 0, 0, 0, big.ctypes.data, n.value, C.byref(n),
+                                offs.ctypes.data, None, None)
+    assert st == 1
+
+
+def test_eval_at_out_of_range_index(ctx):
+    """Every index is range-checked on the device, at any list length: one bad
+    index among 2^21 gives INVALID_ARG and the context stays usable."""
+    pb = workload(1)
+    s = mist.Spec(pb)
+    n = (1 << 21) + 3
+    rng = np.random.default_rng(3)
+    idx = rng.integers(0, s.n_configs, n, dtype=np.uint64)
+    idx[n - 2] = s.n_configs                   # one past the end
+    with pytest.raises(mist.MistError) as ei:
+        gpu_at(ctx, s, idx)
+    assert ei.value.status == 1
+    idx[n - 2] = s.n_configs - 1
+    out = gpu_at(ctx, s, idx[-1000:])
+    assert np.all(out["t"] > 0)
 
 
 def test_device_output_buffers(ctx):

@@ -16,7 +16,7 @@ from oracle import inter
 from oracle.binding import Oracle
 from paper_2503_19050_b200 import mist
 from synth import PRESETS, random_problem, tiny, with_preset, workload
-from tests.parity import compare_dense, compare_frontiers
+from tests.parity import compare_dense, compare_frontiers, frontier_fp_and_bench
 
 pytestmark = pytest.mark.gpu
 
@@ -57,7 +57,7 @@ def test_dense_and_frontier_presets(ctx, name, k):
     n = o.n_configs
     compare_dense(_dense(ctx, s, 0, n), o.eval_range(0, n), pb.name)
     for ykey in (0, 1):
-        pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, s, ykey=ykey, fingerprints=True)
+        pts, offs, fc, fh = frontier_fp_and_bench(ctx, s, ykey=ykey)
         ref = o.sweep(ykey=ykey)
         assert np.array_equal(fc, ref["fp_count"]) and np.array_equal(fh, ref["fp_hash"])
         compare_frontiers(pts, offs, ref["points"], ref["offsets"], label=pb.name)
@@ -68,7 +68,7 @@ def test_dense_and_frontier_presets(ctx, name, k):
 def test_frontier_cfg1_presets(ctx, name):
     pb = with_preset(workload(1), name)
     o, s = Oracle(pb), mist.Spec(pb)
-    pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, s, fingerprints=True)
+    pts, offs, fc, fh = frontier_fp_and_bench(ctx, s)
     ref = o.sweep()
     assert np.array_equal(fc, ref["fp_count"]) and np.array_equal(fh, ref["fp_hash"])
     compare_frontiers(pts, offs, ref["points"], ref["offsets"], label=pb.name)
@@ -79,7 +79,7 @@ def test_frontier_cfg2_presets_sampled_groups(ctx, name):
     # the bench workload through the pilot-filtered sweep; 24 seeded groups checked against the oracle
     pb = with_preset(workload(2), name)
     o, s = Oracle(pb), mist.Spec(pb)
-    pts, offs, fc, fh = mist.mist_pareto_frontier(ctx, s, fingerprints=True)
+    pts, offs, fc, fh = frontier_fp_and_bench(ctx, s)
     rng = np.random.default_rng(7)
     for g in sorted(rng.choice(o.n_groups, size=24, replace=False).tolist()):
         ref = o.sweep(g, g + 1)

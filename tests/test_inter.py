@@ -200,9 +200,12 @@ def test_solver_real_frontier_cfg_tiny():
     _check_plan(plan, keys, thin, 4, 4, want)
 
 
-def test_solver_many_points_per_group():
-    # > 8 candidates per group: the solver first solves a thinned table for its incumbent
-    # (mist_inter.cpp); the optimum must still equal the exhaustive argmin
+@pytest.mark.parametrize("thin", ["0", "1"])
+def test_solver_many_points_per_group(monkeypatch, thin):
+    # > 8 candidates per group: with MIST_INTER_THIN=1 the solver first solves a thinned
+    # table for its incumbent (mist_inter.cpp); the optimum must equal the exhaustive
+    # argmin with and without it
+    monkeypatch.setenv("MIST_INTER_THIN", thin)
     pb = tiny(3, 4, 1, 2, 4, 2)
     keys = _tiny_keys(pb)
     for rep in range(2):
