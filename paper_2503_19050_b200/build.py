@@ -45,12 +45,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "", defs=None) -> str:
     """variant "counters": instrumented copy libmist_counters.so (-DMIST_COUNTERS,
-    event counters printed by the sweep); the product library is untouched."""
-    lib_path, build_dir, defs = LIB, BUILD, []
+    event counters printed by the sweep); any other variant name with `defs`
+    (-D flags): an A/B copy ab/libmist_<variant>.so.  The product library is
+    untouched by variants."""
+    lib_path, build_dir = LIB, BUILD
+    defs = list(defs or [])
     if variant == "counters":
         lib_path, build_dir, defs = os.path.join(PKG, "libmist_counters.so"), BUILD + "_counters", ["-DMIST_COUNTERS"]
+        force = True
+    elif variant:
+        os.makedirs(os.path.join(ROOT, "ab"), exist_ok=True)
+        lib_path, build_dir = os.path.join(ROOT, "ab", f"libmist_{variant}.so"), BUILD + "_" + variant
         force = True
     if not force and not _stale():
         return LIB
@@ -81,5 +88,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True,
-          variant="counters" if "--counters" in sys.argv else "")
+    variant = "counters" if "--counters" in sys.argv else ""
+    if "--variant" in sys.argv:
+        variant = sys.argv[sys.argv.index("--variant") + 1]
+    build(force="--force" in sys.argv, verbose="--quiet" not in sys.argv, variant=variant,
+          defs=[a for a in sys.argv[1:] if a.startswith("-D")])

@@ -37,12 +37,16 @@ cudaError_t launch_precompute(cudaStream_t, int, const DevProblem&, const DevGro
 cudaError_t launch_precompute_segs(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                                    const u64*, int, u64, TupleConst*);
 cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, int);
+cudaError_t launch_pilot_zero(cudaStream_t, int, const DevProblem&, const EvalArgs&);
 size_t eval_smem_bytes(unsigned upt);
 unsigned units_per_tuple(unsigned radix);
 cudaError_t launch_eval_at(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
                            const u64*, long long, u64, unsigned*, double*, double*, double*, uint8_t*);
 // from mist_frontier.cu
 cudaError_t frontier_reduce(cudaStream_t, CandBuf, long long, SortScratch&, u32*, long long*, ReduceStats*);
+// from mist_segfront.cu
+cudaError_t frontier_reduce_seg(cudaStream_t, CandBuf, long long, int, u32*, long long, long long*, ReduceStats*);
+long long seg_scratch_words(long long n, long long ng);
 cudaError_t frontier_group_offsets(cudaStream_t, const u32*, long long, int, int64_t*);
 cudaError_t pack_points(cudaStream_t, CandBuf, long long, mist_point_t*);
 // from mist_sample_dev.cu
@@ -356,7 +360,7 @@ extern "C" void mist_ctx_destroy(mist_ctx_t* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
     for (DevBuf* b : {&ctx->cand_mem, &ctx->sort_mem, &ctx->tuples, &ctx->scan_tmp, &ctx->groups,
-                      &ctx->coef, &ctx->counters, &ctx->fp, &ctx->xfer, &ctx->out, &ctx->foff, &ctx->segs})
+                      &ctx->coef, &ctx->counters, &ctx->fp, &ctx->xfer, &ctx->out, &ctx->foff, &ctx->segs, &ctx->seg})
         release(*b);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -496,10 +500,29 @@ extern "C" mist_status_t mist_eval_stage_costs_at(mist_ctx_t* ctx, const mist_mo
 // ---------------------------------------------------------------------------
 // the sweep
 // ---------------------------------------------------------------------------
-static mist_status_t reduce_now(mist_ctx_t* ctx, long long n, long long* nf) {
+// a9 + a10: group buckets + per-chunk shared-memory sorts (mist_segfront.cu) by
+// default; MIST_REDUCE=radix selects the global radix sort + segmented scan
+// (mist_frontier.cu), which is also the fallback when a group's frontier alone
+// exceeds a chunk.  Both give the same frontier in the same order.
+static bool reduce_radix() {
+    const char* e = getenv("MIST_REDUCE");
+    return e && !strcmp(e, "radix");
+}
+
+static mist_status_t reduce_now(mist_ctx_t* ctx, long long n, int ng, long long* nf) {
     ReduceStats rs;
     int h = ev_begin(ctx, CAT_RED);
-    cudaError_t e = frontier_reduce(ctx->stream, ctx->cand, n, ctx->sort, (u32*)ctx->scan_tmp.p, nf, &rs);
+    cudaError_t e = cudaErrorNotSupported;
+    if (!reduce_radix()) {
+        // sized for the largest n the candidate buffer can hand over (cap / 2), so that
+        // a step whose candidate count tops the earlier ones does not re-allocate
+        const long long words = seg_scratch_words(std::max(n, ctx->cand.cap / 2), ng);
+        CK(ensure(ctx->seg, sizeof(u32) * (size_t)words), "alloc seg scratch");
+        e = frontier_reduce_seg(ctx->stream, ctx->cand, n, ng, (u32*)ctx->seg.p, words, nf, &rs);
+        if (e == cudaErrorNotSupported) cudaGetLastError();
+    }
+    if (e == cudaErrorNotSupported)
+        e = frontier_reduce(ctx->stream, ctx->cand, n, ctx->sort, (u32*)ctx->scan_tmp.p, nf, &rs);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "frontier_reduce");
     ev_end(ctx, h);
     ctx->stats.kernel_launches += rs.launches;
@@ -543,7 +566,7 @@ static mist_status_t write_count(mist_ctx_t* ctx, SweepCtx& S, long long v) {
 // Reduce the buffer to its exact frontier; the frontier becomes the staircase filter.
 static mist_status_t reduce_buffer(mist_ctx_t* ctx, SweepCtx& S) {
     long long nf = 0;
-    mist_status_t st = reduce_now(ctx, S.count, &nf);
+    mist_status_t st = reduce_now(ctx, S.count, S.pp->ng, &nf);
     if (st != MIST_OK) return st;
     st = write_count(ctx, S, nf);
     if (st != MIST_OK) return st;
@@ -697,6 +720,8 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
         }
     }
     for (auto& nv : levels) nv = std::min(nv, Q + 1);
+    const char* zenv = getenv("MIST_PILOT_ZERO");
+    const bool zero_pilot = !(zenv && zenv[0] == '0');
     const char* env = getenv("MIST_PILOT");
     const bool pilot = !(env && env[0] == '0') && Q >= 2 && total_runs >= (1ull << 22);
     for (const auto& ch : chunks) {
@@ -727,6 +752,32 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
         ctx->stats.kernel_launches += 1;
         ev_end(ctx, h);
         const TupleConst* tup = (const TupleConst*)ctx->tuples.p;
+        if (pilot && zero_pilot && pp.P.ykey == 0) {
+            // zero-offload pilot (R7's y = 0 points): <= one candidate per group per warp of tuples
+            for (u64 a = 0; a < nT;) {
+                if (S.count > S.C / 4) {
+                    st = reduce_buffer(ctx, S);
+                    if (st != MIST_OK) return st;
+                }
+                const u64 b = std::min<u64>(nT, a + (u64)(S.C / 4));
+                EvalArgs A;
+                std::memset(&A, 0, sizeof(A));
+                A.tuples = tup + a;
+                A.n_units = b - a;
+                A.cand = ctx->cand;
+                A.cand_count = S.d_count;
+                const int hz = ev_begin(ctx, CAT_PILOT);
+                CK(launch_pilot_zero(ctx->stream, ctx->device, pp.P, A), "pilot zero");
+                ev_end(ctx, hz);
+                ctx->stats.kernel_launches += 1;
+                long long c = 0;
+                st = read_count(ctx, S, &c);
+                if (st != MIST_OK) return st;
+                S.count = c;
+                ctx->stats.pilot_configs += (b - a) * (u64)(pp.P.kmax[3] + 1);
+                a = b;
+            }
+        }
         if (pilot) {
             // pilot sweeps of sub-grids seed an exact staircase filter (their points are
             // real feasible configs of the same groups, so anything they beat is beaten)
@@ -760,7 +811,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
 #endif
     }
     long long nf = 0;
-    st = reduce_now(ctx, S.count, &nf);
+    st = reduce_now(ctx, S.count, pp.ng, &nf);
     if (st != MIST_OK) return st;
     ctx->stats.configs_evaluated += n_tuples * pp.R;
     ctx->stats.frontier_points = (uint64_t)nf;
@@ -768,7 +819,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     return MIST_OK;
 }
 
-static mist_status_t merge_ranks(mist_ctx_t* ctx, long long nf_local, long long* nf_out) {
+static mist_status_t merge_ranks(mist_ctx_t* ctx, int ng, long long nf_local, long long* nf_out) {
     ncclComm_t comm = (ncclComm_t)ctx->nccl;
     int h = ev_begin(ctx, CAT_MERGE);
     // 1) all-gather counts
@@ -804,7 +855,7 @@ static mist_status_t merge_ranks(mist_ctx_t* ctx, long long nf_local, long long*
     ctx->stats.kernel_launches += 1 + ctx->world;
     ev_end(ctx, h);
     long long nf = 0;
-    st = reduce_now(ctx, total, &nf);
+    st = reduce_now(ctx, total, ng, &nf);
     if (st != MIST_OK) return st;
     *nf_out = nf;
     return MIST_OK;
@@ -841,7 +892,7 @@ static mist_status_t frontier_device(mist_ctx_t* ctx, const Prepared& pp, uint64
         if (st != MIST_OK) return st;
     }
     if (ctx->nccl && ctx->world > 1) {
-        st = merge_ranks(ctx, nf, &nf);
+        st = merge_ranks(ctx, pp.ng, nf, &nf);
         if (st != MIST_OK) return st;
         if (want_fp) {
             ncclResult_t r = ncclAllReduce(ctx->fp.p, ctx->fp.p, 2 * (size_t)pp.ng, ncclUint64, ncclSum,
@@ -1090,7 +1141,7 @@ extern "C" mist_status_t mist_frontier_points(mist_ctx_t* ctx, const mist_point_
     if (bad) return fail(ctx, MIST_ERR_INVALID_ARG, "group out of range or t negative / non-finite");
     const int htot = ev_begin(ctx, CAT_TOTAL);
     long long nf = 0;
-    st = reduce_now(ctx, n, &nf);
+    st = reduce_now(ctx, n, (int)n_groups, &nf);
     if (st != MIST_OK) return st;
     CK(ensure(ctx->out, sizeof(mist_point_t) * (size_t)std::max<long long>(1, nf) +
                             sizeof(int64_t) * ((size_t)n_groups + 1)), "alloc out");

@@ -185,10 +185,32 @@ typedef double2 FGRow[4];
 // min/max without fmin/fmax's NaN handling (no NaN can occur here): DSETP + 2 selects
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
-template <bool UNIT>
-__device__ __forceinline__ double pred_intf(double x0, double x1, double x2, double x3,
-                                            const FGRow* __restrict__ FG) {
-    if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));   // unit factors: perfect overlap = max
+// Code-size knobs for A/B builds (-DMIST_NI_*): one shared, called copy instead
+// of an inlined copy per call site (the eval kernel's SASS is ~127 KB against a
+// 32 KB L1.5 instruction cache).
+#ifdef MIST_NI_PRED
+#define MIST_PRED_ATTR __noinline__
+#else
+#define MIST_PRED_ATTR __forceinline__
+#endif
+#ifdef MIST_NI_LB
+#define MIST_LB_ATTR __noinline__
+#else
+#define MIST_LB_ATTR __forceinline__
+#endif
+#ifdef MIST_NI_DLB
+#define MIST_DLB_ATTR __noinline__
+#else
+#define MIST_DLB_ATTR __forceinline__
+#endif
+#ifdef MIST_NI_CUT
+#define MIST_CUT_ATTR __noinline__
+#else
+#define MIST_CUT_ATTR
+#endif
+
+__device__ MIST_PRED_ATTR double pred_intf_gen(double x0, double x1, double x2, double x3,
+                                               const FGRow* __restrict__ FG) {
     double T = 0.0;
 #pragma unroll
     for (int round = 0; round < 3; ++round) {
@@ -209,6 +231,13 @@ __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, dou
         T += ov;
     }
     return T + (((x0 + x1) + x2) + x3);
+}
+
+template <bool UNIT>
+__device__ __forceinline__ double pred_intf(double x0, double x1, double x2, double x3,
+                                            const FGRow* __restrict__ FG) {
+    if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));   // unit factors: perfect overlap = max
+    return pred_intf_gen(x0, x1, x2, x3, FG);
 }
 
 // Loop nest of one thread: unit (kW, kA) -> run kG -> config kO.
@@ -372,10 +401,16 @@ __device__ __forceinline__ double d_kO(const TupleConst& tc, const UnitState& us
 // at least that long again, so T >= x_m + ov (1 - 1/F_m) for every m in S (and
 // T >= ov for the zero channels, which have g = 0 in the table).  Unit factors
 // make Alg. 1 the max itself, so only R4 is used there.
+__device__ MIST_LB_ATTR double lb_row_gen(double x0, double x1, double x2, double x3, const FGRow* FG);
+
 template <bool UNIT>
 __device__ __forceinline__ double lb_row(double x0, double x1, double x2, double x3, const FGRow* FG) {
+    if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));
+    return lb_row_gen(x0, x1, x2, x3, FG);
+}
+
+__device__ MIST_LB_ATTR double lb_row_gen(double x0, double x1, double x2, double x3, const FGRow* FG) {
     const double mx = dmax(dmax(x0, x1), dmax(x2, x3));
-    if (UNIT) return mx;
     const unsigned pat = (unsigned)(x0 != 0.0) | ((unsigned)(x1 != 0.0) << 1) | ((unsigned)(x2 != 0.0) << 2) |
                          ((unsigned)(x3 != 0.0) << 3);
     if (__popc(pat) < 2) return mx;
@@ -404,7 +439,7 @@ __device__ __forceinline__ bool fp_pattern_fixed(const TupleConst& tc, const Run
 // Lower bound of d at config kO: rs.dbase + sum count * (lb_row(F') - T(F)) over the blocks.
 // `scale` bounds the magnitudes summed, for a rounding margin.
 template <bool UNIT>
-__device__ __forceinline__ double d_lower_bound(const TupleConst& tc, const UnitState& us, const RunState& rs,
+__device__ MIST_DLB_ATTR double d_lower_bound(const TupleConst& tc, const UnitState& us, const RunState& rs,
                                                 double kO, const FGRow* FG, double& scale) {
     double lb = rs.dbase, sc = fabs(rs.dbase);
     const double H = rs.FpH_L + kO * tc.L.sOh;
@@ -463,7 +498,7 @@ __device__ __forceinline__ double run_t_lb(const TupleConst& tc, const UnitState
 // is non-increasing in kG and kO under the kG-suffix property, R2').  The t bound
 // carries a 1e-12 relative margin for the rounding of R4/R5 against Alg. 1.
 template <bool UNIT>
-__device__ unsigned run_cut(const DevProblem& P, const TupleConst& tc, const UnitState& us, unsigned kW, unsigned kA,
+__device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst& tc, const UnitState& us, unsigned kW, unsigned kA,
                             unsigned g0, unsigned gend, const FGRow* FG, const double* ft, const double* fy,
                             long long lo, long long hi) {
     if (lo >= hi) return gend;
@@ -1089,6 +1124,71 @@ k_eval_q(DevProblem P, EvalArgs A) {
     }    flush_ctr(A, ctr, lane);
 }
 
+// Zero-offload pilot (ykey = d; feeds R7).  A config can have d = 0 only without
+// first-microbatch extras: WO = GO = OO = 0 (O6's F' adds OO, GO and WO traffic)
+// and no last-microbatch collective or post-update gather (z = 3 or DP = 1).
+// The sub-grid pilot samples AO at a few values only, so its y = 0 point can sit
+// well right of the group's true one.  One thread per tuple walks every admitted
+// kA of (kW, kG, kO) = (0, 0, 0), keeps the feasible config of least (t, idx)
+// with d = 0, and the warp emits one candidate per group (leader of the group's
+// lanes).  The candidates are real feasible configs, so any point they beat is
+// beaten (O10): the staircase they join stays exact.
+template <bool UNIT>
+__global__ void __launch_bounds__(128)
+k_pilot_zero(DevProblem P, EvalArgs A) {
+    __shared__ FGRow FG[16];
+    load_fg(P, FG, threadIdx.x);
+    __syncthreads();
+    const double Q = P.Q;
+    const unsigned lane = threadIdx.x & 31;
+    const u64 nT = A.n_units;
+    for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < nT;
+         base += (u64)gridDim.x * blockDim.x) {
+        const u64 T = base + lane;
+        bool has = false;
+        double bt = CUDART_INF, bm = 0.0;
+        u64 bi = 0;
+        unsigned grp = 0xffffffffu;
+        if (T < nT) {
+            const TupleConst& tc = A.tuples[T];
+            grp = (unsigned)tc.group;
+            const bool bp_eq = tc.L.N_Bp == tc.L.N_B && (!tc.first || tc.E.N_Bp == tc.E.N_B) &&
+                               (!tc.last || tc.H.N_Bp == tc.H.N_B);
+            const bool fp_eq = tc.L.N_Fp == tc.L.N_F && (!tc.first || tc.E.N_Fp == tc.E.N_F) &&
+                               (!tc.last || tc.H.N_Fp == tc.H.N_F);
+            if (bp_eq && fp_eq && !(tc.DMB < 0.0)) {
+                for (int kA = 0; kA <= P.kmax[3]; ++kA) {
+                    RunState rs;
+                    run_memory(tc, 0.0, 0.0, (double)kA, Q, rs);
+                    const double memD = mem_kO(tc, rs, 0.0, Q);
+                    if (!(memD <= tc.DMB)) continue;           // Eq. 4
+                    UnitState us;
+                    unit_forward<UNIT>(tc, 0.0, (double)kA, FG, us);
+                    run_backward<UNIT>(tc, us, 0.0, 0.0, (double)kA, FG, rs);
+                    if (!(rs.t < bt)) continue;                 // ties: the smaller kA (idx) stays
+                    if (d_kO<UNIT>(tc, us, rs, 0.0, FG) != 0.0) continue;
+                    has = true; bt = rs.t; bm = memD / tc.D; bi = tc.idx_base + (u64)kA;
+                }
+            }
+        }
+        // per group of the warp's lanes: the least (t, idx)
+        const unsigned peers = __match_any_sync(0xffffffffu, grp);
+        double t = has ? bt : CUDART_INF;
+        u64 ix = has ? bi : ~0ull;
+        double m = bm;
+        for (unsigned rest = peers; rest;) {
+            const int src = __ffs(rest) - 1;
+            rest &= rest - 1;
+            const double ot = __shfl_sync(peers, t, src);
+            const u64 oi = __shfl_sync(peers, ix, src);
+            const double om = __shfl_sync(peers, m, src);
+            if (ot < t || (ot == t && oi < ix)) { t = ot; ix = oi; m = om; }
+        }
+        const bool emit = (int)lane == __ffs(peers) - 1 && ix != ~0ull;
+        warp_emit(emit, t, 0.0, m, ix, grp, A, lane);
+    }
+}
+
 // Arbitrary index list (test hook): one thread per index, tuple built in registers.
 template <bool UNIT>
 __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int ng,
@@ -1294,6 +1394,19 @@ cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const 
     if (mode == 1) return launch_eval_t<false, 1, 256, 2>(st, device, P, A);
     if (mode == 2) return launch_eval_t<false, 2, 256, 2>(st, device, P, A);
     return launch_frontier_eval<false>(st, device, P, A);
+}
+
+cudaError_t launch_pilot_zero(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
+    if (A.n_units == 0) return cudaSuccess;
+    const int threads = 128;
+    u64 blocks = (A.n_units + threads - 1) / threads;
+    const u64 cap = (u64)sm_count(device) * 8;
+    if (blocks > cap) blocks = cap;
+    if (P.unit_factors)
+        k_pilot_zero<true><<<(unsigned)blocks, threads, 0, st>>>(P, A);
+    else
+        k_pilot_zero<false><<<(unsigned)blocks, threads, 0, st>>>(P, A);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_eval_at(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,

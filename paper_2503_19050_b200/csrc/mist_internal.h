@@ -151,6 +151,7 @@ struct mist_ctx {
     mist_stats_t stats{};
     // device scratch (grown on demand, freed by mist_ctx_destroy)
     mist::DevBuf cand_mem, sort_mem, tuples, scan_tmp, groups, coef, counters, fp, xfer, out, foff, segs;
+    mist::DevBuf seg;   // scratch of the group-bucket frontier reduction (mist_segfront.cu)
     mist::CandBuf cand;            // views into cand_mem
     mist::SortScratch sort;        // views into sort_mem
     // cached last frontier (for BUFFER_TOO_SMALL retries)

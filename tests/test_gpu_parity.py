@@ -280,18 +280,29 @@ def test_invalid_groups_rejected(ctx):
     assert ei.value.status == 1
 
 
-@pytest.mark.parametrize("seed", range(6))
-def test_frontier_points_vs_oracle(ctx, seed):
-    """a9 + a10 alone: the GPU radix sort + segmented scan on random point sets
-    (heavy ties in t and y, several digit passes, many groups, ragged sizes)
-    equals the oracle's O(k^2)/sort-scan frontier of the same points, bit for bit."""
+@pytest.mark.parametrize("reduce", ["seg", "radix"])
+@pytest.mark.parametrize("seed", range(10))
+def test_frontier_points_vs_oracle(ctx, seed, reduce, monkeypatch):
+    """a9 + a10 alone, on both reductions (group buckets + shared-memory chunk
+    sorts, the default; global radix sort + segmented scan, MIST_REDUCE=radix):
+    random point sets (heavy ties in t and y, many binades, many groups, ragged
+    sizes; seeds 6-8: a few groups of up to 1e5 points, so groups span many
+    2048-record chunks and several levels; seed 9: one group whose frontier alone
+    exceeds a chunk, which the bucket path hands to the radix path) equal the
+    oracle's O(k^2)/sort-scan frontier of the same points, bit for bit."""
     from oracle.binding import frontier_points as orc_frontier
+    monkeypatch.setenv("MIST_REDUCE", reduce)
     rng = np.random.default_rng(seed)
     n = int(rng.integers(1, 300_000)) if seed else 5
-    ng = int(rng.integers(1, 2000))
+    ng = int(rng.integers(1, 2000)) if seed < 6 else int(rng.integers(1, 9))
+    if seed == 9:
+        n, ng = 6000, 1
     g = np.sort(rng.integers(0, ng, n)).astype(np.int32) if seed % 2 else rng.integers(0, ng, n).astype(np.int32)
     pts = np.zeros(n, dtype=mist.POINT_DTYPE)
-    if seed % 3 == 0:      # few distinct values: long equal-t runs and y ties
+    if seed == 9:          # every point on the frontier: t rises, y falls
+        pts["t"] = rng.permutation(n) + 1.0
+        pts["y"] = n + 1.0 - pts["t"]
+    elif seed % 3 == 0:    # few distinct values: long equal-t runs and y ties
         pts["t"] = rng.integers(0, 50, n) * 0.125
         pts["y"] = rng.integers(0, 50, n) * 0.5
     else:                  # full-precision doubles across many binades
@@ -300,6 +311,8 @@ def test_frontier_points_vs_oracle(ctx, seed):
     pts["idx"] = rng.permutation(n * 4)[:n].astype(np.uint64)
     pts["mem"] = rng.uniform(0, 1e10, n)
     fr, offs = mist.mist_frontier_points(ctx, pts, g, ng)
+    if seed == 9:
+        assert len(fr) == n
     for q in range(ng):
         sel = g == q
         op = np.zeros(int(sel.sum()), dtype=ORC_POINT)
