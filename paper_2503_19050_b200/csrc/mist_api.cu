@@ -777,6 +777,12 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
                 ctx->stats.pilot_configs += (b - a) * (u64)(pp.P.kmax[3] + 1);
                 a = b;
             }
+            // its y = 0 points become the staircase of the sub-grid levels (R7 and the
+            // staircase filter run there too)
+            if (S.count > 0) {
+                st = reduce_buffer(ctx, S);
+                if (st != MIST_OK) return st;
+            }
         }
         if (pilot) {
             // pilot sweeps of sub-grids seed an exact staircase filter (their points are

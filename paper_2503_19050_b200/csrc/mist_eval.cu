@@ -233,10 +233,20 @@ __device__ MIST_PRED_ATTR double pred_intf_gen(double x0, double x1, double x2, 
     return T + (((x0 + x1) + x2) + x3);
 }
 
-template <bool UNIT>
+// one shared, called copy for the rows evaluated once per unit or run (F, B, B'):
+// the per-config rows (F', bounds) stay inlined in the kO loop
+__device__ __noinline__ double pred_intf_ni(double x0, double x1, double x2, double x3,
+                                            const FGRow* __restrict__ FG) {
+    return pred_intf_gen(x0, x1, x2, x3, FG);
+}
+
+template <bool UNIT, bool NI = false>
 __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, double x3,
                                             const FGRow* __restrict__ FG) {
     if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));   // unit factors: perfect overlap = max
+#ifdef MIST_SEL_NI
+    if (NI) return pred_intf_ni(x0, x1, x2, x3, FG);
+#endif
     return pred_intf_gen(x0, x1, x2, x3, FG);
 }
 
@@ -305,17 +315,17 @@ __device__ __forceinline__ void unit_forward(const TupleConst& tc, double kW, do
     us.FD_L0 = kA * tc.L.sAd;
     us.FD_L1 = kA * tc.L.sAd1;
     us.TF_L0 = us.TF_L1 = us.TF_E = us.TF_H = 0.0;
-    if (tc.nl0 > 0.0) us.TF_L0 = pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L0, FG);
-    if (tc.nl1 > 0.0) us.TF_L1 = pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L1, FG);
+    if (tc.nl0 > 0.0) us.TF_L0 = pred_intf<UNIT, true>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L0, FG);
+    if (tc.nl1 > 0.0) us.TF_L1 = pred_intf<UNIT, true>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L1, FG);
     if (tc.first) {
         us.FH_E = kW * tc.E.sWh;
         us.FD_E = kA * tc.E.sAd;
-        us.TF_E = pred_intf<UNIT>(tc.E.C_F, tc.E.N_F, us.FH_E, us.FD_E, FG);
+        us.TF_E = pred_intf<UNIT, true>(tc.E.C_F, tc.E.N_F, us.FH_E, us.FD_E, FG);
     }
     if (tc.last) {
         us.FH_H = kW * tc.H.sWh;
         us.FD_H = kA * tc.H.sAd;
-        us.TF_H = pred_intf<UNIT>(tc.H.C_F, tc.H.N_F, us.FH_H, us.FD_H, FG);
+        us.TF_H = pred_intf<UNIT, true>(tc.H.C_F, tc.H.N_F, us.FH_H, us.FD_H, FG);
     }
 }
 
@@ -339,8 +349,8 @@ __device__ __noinline__ double block_backward(const BlockConst& b, bool r1, doub
     const double sAh = r1 ? b.sAh1 : b.sAh;
     const double CB = r1 ? b.C_B1 : b.C_B;                   // a checkpointed layer recomputes (L17)
     const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
-    const double TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, FG);
-    dBp = (b.N_Bp == b.N_B) ? 0.0 : pred_intf<UNIT>(CB, b.N_Bp, BH, BD, FG) - TB;
+    const double TB = pred_intf<UNIT, true>(CB, b.N_B, BH, BD, FG);
+    dBp = (b.N_Bp == b.N_B) ? 0.0 : pred_intf<UNIT, true>(CB, b.N_Bp, BH, BD, FG) - TB;
     return TB;
 }
 
@@ -403,9 +413,16 @@ __device__ __forceinline__ double d_kO(const TupleConst& tc, const UnitState& us
 // make Alg. 1 the max itself, so only R4 is used there.
 __device__ MIST_LB_ATTR double lb_row_gen(double x0, double x1, double x2, double x3, const FGRow* FG);
 
-template <bool UNIT>
+__device__ __noinline__ double lb_row_ni(double x0, double x1, double x2, double x3, const FGRow* FG) {
+    return lb_row_gen(x0, x1, x2, x3, FG);
+}
+
+template <bool UNIT, bool NI = false>
 __device__ __forceinline__ double lb_row(double x0, double x1, double x2, double x3, const FGRow* FG) {
     if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));
+#ifdef MIST_SEL_NI
+    if (NI) return lb_row_ni(x0, x1, x2, x3, FG);
+#endif
     return lb_row_gen(x0, x1, x2, x3, FG);
 }
 
@@ -475,7 +492,7 @@ __device__ __forceinline__ double lb_backward(const BlockConst& b, bool r1, doub
     const double CB = r1 ? b.C_B1 : b.C_B;
     const double BH = FH + kG * b.sGh + kA * (r1 ? b.sAh1 : b.sAh), BD = kG * b.sGd;
     if (kG == 0.0) return dmax(dmax(CB, b.N_B), dmax(BH, BD));
-    return lb_row<UNIT>(CB, b.N_B, BH, BD, FG);
+    return lb_row<UNIT, true>(CB, b.N_B, BH, BD, FG);
 }
 
 template <bool UNIT>
@@ -500,12 +517,13 @@ __device__ __forceinline__ double run_t_lb(const TupleConst& tc, const UnitState
 template <bool UNIT>
 __device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst& tc, const UnitState& us, unsigned kW, unsigned kA,
                             unsigned g0, unsigned gend, const FGRow* FG, const double* ft, const double* fy,
-                            long long lo, long long hi) {
+                            long long lo, long long hi, const unsigned* vals = nullptr) {
+    // vals (pilot sub-grid): runs are indices into vals[] (ascending kG values)
     if (lo >= hi) return gend;
     const double dkA = kA;
     double ymin = 0.0;                         // ykey = d: y >= 0
     if (P.ykey) {
-        if (!(tc.mG >= tc.gb_k)) return gend;  // mem not monotone in kG: no cut
+        if (vals || !(tc.mG >= tc.gb_k)) return gend;   // mem not monotone in kG / sub-grid: no cut
         RunState rm;
         run_memory(tc, (double)kW, (double)(gend - 1), dkA, (double)P.Q, rm);
         ymin = mem_kO(tc, rm, (double)P.kmax[2], (double)P.Q) / tc.D;
@@ -513,7 +531,7 @@ __device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst&
         return gend;                           // no y = 0 point: nothing below every d
     }
     auto cut = [&](unsigned g) -> bool {
-        const double lb = run_t_lb<UNIT>(tc, us, (double)g, dkA, FG) * (1.0 - 1e-12);
+        const double lb = run_t_lb<UNIT>(tc, us, (double)(vals ? vals[g] : g), dkA, FG) * (1.0 - 1e-12);
         if (!P.ykey) return ft[hi - 1] < lb;
         long long a = lo, b = hi;              // points with t < lb: [lo, a)
         while (a < b) {
@@ -776,6 +794,11 @@ k_eval(DevProblem P, EvalArgs A) {
         const unsigned grp = tc.group;
         UnitState us;
         if (active) unit_forward<UNIT>(tc, dkW, dkA, FG, us);
+        // R7 (frontier and pilot modes): runs ig >= icut are beaten by the staircase on t alone
+        unsigned icut = radix;
+        if (MODE != 1 && active && A.f_off && !A.fp && !A.no_r7)
+            icut = run_cut<UNIT>(P, tc, us, kW, kA, 0u, radix, FG, A.f_t, A.f_y, A.f_off[grp], A.f_off[grp + 1],
+                                 MODE == 2 ? A.vals : nullptr);
         // phase rows evaluated by this thread (PredINTF calls), for the roofline's algorithmic count
         const unsigned nrows = (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
                                (unsigned)(tc.last != 0);
@@ -791,7 +814,7 @@ k_eval(DevProblem P, EvalArgs A) {
             double et = 0.0, ey = 0.0, em = 0.0;
             u64 ei = 0;
             const unsigned kG = (MODE == 2) ? A.vals[ig] : ig;
-            if (active && (MODE == 1 || kG <= (unsigned)P.kmax[1])) {
+            if (active && ig < icut && (MODE == 1 || kG <= (unsigned)P.kmax[1])) {
                 const double dkG = kG;
                 RunState rs;
                 run_memory(tc, dkW, dkG, dkA, Q, rs);

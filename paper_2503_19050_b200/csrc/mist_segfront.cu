@@ -40,7 +40,7 @@ long long scan_tmp_words(long long n);
 constexpr int kChunk = 2048;          // records per chunk (one CTA)
 constexpr int kChunkThreads = 256;
 constexpr int kPerThread = kChunk / kChunkThreads;
-constexpr int kChunkSmem = kChunk * (8 + 8 + 8 + 2);   // t, y, idx, permutation
+constexpr int kChunkSmem = (kChunk + 1) * (8 + 8 + 8) + kChunk * 2;   // t, y, idx (+ sentinel), permutation
 
 // per candidate: rank within its group; counts per group (cnt pre-zeroed)
 __global__ void k_seg_count(const u32* __restrict__ group, long long n, u32* __restrict__ cnt,
@@ -95,39 +95,85 @@ __device__ __forceinline__ int chunk_group(const u32* __restrict__ co, int ng, u
     return lo;
 }
 
+__device__ __forceinline__ u32 block_excl_count(u32 mine, u32* s_wcnt, u32& all) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u32 pre = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+    }
+    if (lane == 31) s_wcnt[w] = pre;
+    __syncthreads();
+    u32 before = pre - mine;
+    all = 0;
+    for (int q = 0; q < kChunkThreads / 32; ++q) {
+        const u32 v = s_wcnt[q];
+        before += q < w ? v : 0u;
+        all += v;
+    }
+    __syncthreads();                                      // s_wcnt free for the next use
+    return before;
+}
+
 // One CTA per chunk (grid-stride over *nchunks).  The chunk's records are
 // X[goff[g] + j*kChunk, +len); its frontier goes back to the chunk's start and
-// its size to nf[c].
+// its size to nf[c].  Prefilter: every thread drops the records of its own 8
+// that another of its 8 beats (O10, pairwise), so only the survivors are sorted.
 __global__ void __launch_bounds__(kChunkThreads)
 k_chunk_front(CandBuf X, const u32* __restrict__ cnt, const u32* __restrict__ goff, const u32* __restrict__ co,
               int ng, const u32* __restrict__ nchunks, u32* __restrict__ nf) {
-    extern __shared__ __align__(16) double s_t[];     // [kChunk] t, then y, idx, permutation
-    double* s_y = s_t + kChunk;
-    u64* s_i = reinterpret_cast<u64*>(s_y + kChunk);
-    unsigned short* s_p = reinterpret_cast<unsigned short*>(s_i + kChunk);
+    extern __shared__ __align__(16) double s_t[];     // [kChunk + 1] t, then y, idx; permutation [kChunk]
+    double* s_y = s_t + (kChunk + 1);
+    u64* s_i = reinterpret_cast<u64*>(s_y + (kChunk + 1));
+    unsigned short* s_p = reinterpret_cast<unsigned short*>(s_i + (kChunk + 1));
     __shared__ double s_wmin[kChunkThreads / 32];
     __shared__ u32 s_wcnt[kChunkThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const u32 total = *nchunks;
     if (blockIdx.x == 0 && tid == 0) nf[total] = 0;      // the scan runs over total + 1 entries
+    if (tid == 0) { s_t[kChunk] = CUDART_INF; s_y[kChunk] = CUDART_INF; s_i[kChunk] = ~0ull; }   // sentinel
     for (u32 c = blockIdx.x; c < total; c += gridDim.x) {
         const int g = chunk_group(co, ng, c);
         const u32 j = c - co[g];
         const u32 start = goff[g] + j * kChunk;
         const int len = (int)min((u32)kChunk, cnt[g] - j * kChunk);
-        int P = 32;
-        while (P < len) P <<= 1;
         __syncthreads();                                  // previous chunk done with smem
-        for (int k = tid; k < P; k += kChunkThreads) {
-            if (k < len) {
-                s_t[k] = X.t[start + k]; s_y[k] = X.y[start + k]; s_i[k] = X.idx[start + k];
-            } else {
-                s_t[k] = CUDART_INF; s_y[k] = CUDART_INF; s_i[k] = ~0ull;
-            }
-            s_p[k] = (unsigned short)k;
+        for (int k = tid; k < len; k += kChunkThreads) {
+            s_t[k] = X.t[start + k]; s_y[k] = X.y[start + k]; s_i[k] = X.idx[start + k];
         }
         __syncthreads();
-        // bitonic sort of the permutation by (t, y, idx) ascending
+        // thread-local prefilter over records k0 .. k0 + 7
+        const int k0 = tid * kPerThread;
+        double tt[kPerThread], yy[kPerThread];
+        u64 ii[kPerThread];
+#pragma unroll
+        for (int q = 0; q < kPerThread; ++q) {
+            const bool ok = k0 + q < len;
+            tt[q] = ok ? s_t[k0 + q] : CUDART_INF;
+            yy[q] = ok ? s_y[k0 + q] : CUDART_INF;
+            ii[q] = ok ? s_i[k0 + q] : ~0ull;
+        }
+        unsigned alive = 0;
+#pragma unroll
+        for (int q = 0; q < kPerThread; ++q) {
+            bool beaten = !(k0 + q < len);
+#pragma unroll
+            for (int r = 0; r < kPerThread; ++r)
+                if (r != q)
+                    beaten |= tt[r] <= tt[q] && yy[r] <= yy[q] && (tt[r] < tt[q] || yy[r] < yy[q] || ii[r] < ii[q]);
+            if (!beaten) alive |= 1u << q;
+        }
+        u32 ns;
+        u32 pos = block_excl_count((u32)__popc(alive), s_wcnt, ns);
+#pragma unroll
+        for (int q = 0; q < kPerThread; ++q)
+            if ((alive >> q) & 1u) s_p[pos++] = (unsigned short)(k0 + q);
+        int P = 32;
+        while (P < (int)ns) P <<= 1;
+        for (int k = (int)ns + tid; k < P; k += kChunkThreads) s_p[k] = (unsigned short)kChunk;   // sentinel
+        __syncthreads();
+        // bitonic sort of the survivors by (t, y, idx) ascending
         for (int size = 2; size <= P; size <<= 1) {
             for (int stride = size >> 1; stride > 0; stride >>= 1) {
                 for (int q = tid; q < P / 2; q += kChunkThreads) {
@@ -141,15 +187,14 @@ k_chunk_front(CandBuf X, const u32* __restrict__ cnt, const u32* __restrict__ go
                 __syncthreads();
             }
         }
-        // frontier flags: y_k < min over earlier y (exclusive prefix min); thread owns
-        // kPerThread consecutive sorted positions
-        const int k0 = tid * kPerThread;
+        // frontier flags over sorted positions [0, ns): y_k < min over earlier y
+        // (exclusive prefix min); thread owns kPerThread consecutive positions
         double ys[kPerThread];
         double m = CUDART_INF;
 #pragma unroll
         for (int q = 0; q < kPerThread; ++q) {
             const int k = k0 + q;
-            ys[q] = k < len ? s_y[s_p[k]] : CUDART_INF;
+            ys[q] = k < (int)ns ? s_y[s_p[k]] : CUDART_INF;
             m = fmin(m, ys[q]);
         }
         double incl = m;                                  // warp inclusive min-scan of thread minima
@@ -166,25 +211,11 @@ k_chunk_front(CandBuf X, const u32* __restrict__ cnt, const u32* __restrict__ go
         unsigned flags = 0;
 #pragma unroll
         for (int q = 0; q < kPerThread; ++q) {
-            if (k0 + q < len && ys[q] < excl) flags |= 1u << q;
+            if (k0 + q < (int)ns && ys[q] < excl) flags |= 1u << q;
             excl = fmin(excl, ys[q]);
         }
-        // positions of the flagged records: block exclusive sum of the flag counts
-        const u32 mine = (u32)__popc(flags);
-        u32 pre = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 v = __shfl_up_sync(0xffffffffu, pre, o);
-            if (lane >= o) pre += v;
-        }
-        if (lane == 31) s_wcnt[w] = pre;
-        __syncthreads();
-        u32 before = pre - mine, all = 0;
-        for (int q = 0; q < kChunkThreads / 32; ++q) {
-            const u32 v = s_wcnt[q];
-            before += q < w ? v : 0u;
-            all += v;
-        }
+        u32 all;
+        const u32 before = block_excl_count((u32)__popc(flags), s_wcnt, all);
         // read the kept records' mem before any write into the chunk (in place)
         double mm[kPerThread];
 #pragma unroll
