@@ -615,7 +615,7 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     for (unsigned i = 0; i < nv && i < 16; ++i) A.vals[i] = vals[i];
     {
         const char* e = getenv("MIST_R7");
-        A.no_r7 = (e && e[0] == '0') ? 1 : 0;
+        A.no_r7 = (e && e[0] == '0') ? 1 : (e && !strcmp(e, "unit")) ? 2 : 0;
     }
     if ((mode == 0 || mode == 2) && S.filter) {
         A.f_t = ctx->cand.t;

@@ -193,11 +193,6 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 #else
 #define MIST_PRED_ATTR __forceinline__
 #endif
-#ifdef MIST_NI_LB
-#define MIST_LB_ATTR __noinline__
-#else
-#define MIST_LB_ATTR __forceinline__
-#endif
 #ifdef MIST_NI_DLB
 #define MIST_DLB_ATTR __noinline__
 #else
@@ -233,20 +228,10 @@ __device__ MIST_PRED_ATTR double pred_intf_gen(double x0, double x1, double x2, 
     return T + (((x0 + x1) + x2) + x3);
 }
 
-// one shared, called copy for the rows evaluated once per unit or run (F, B, B'):
-// the per-config rows (F', bounds) stay inlined in the kO loop
-__device__ __noinline__ double pred_intf_ni(double x0, double x1, double x2, double x3,
-                                            const FGRow* __restrict__ FG) {
-    return pred_intf_gen(x0, x1, x2, x3, FG);
-}
-
-template <bool UNIT, bool NI = false>
+template <bool UNIT>
 __device__ __forceinline__ double pred_intf(double x0, double x1, double x2, double x3,
                                             const FGRow* __restrict__ FG) {
     if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));   // unit factors: perfect overlap = max
-#ifdef MIST_SEL_NI
-    if (NI) return pred_intf_ni(x0, x1, x2, x3, FG);
-#endif
     return pred_intf_gen(x0, x1, x2, x3, FG);
 }
 
@@ -315,17 +300,17 @@ __device__ __forceinline__ void unit_forward(const TupleConst& tc, double kW, do
     us.FD_L0 = kA * tc.L.sAd;
     us.FD_L1 = kA * tc.L.sAd1;
     us.TF_L0 = us.TF_L1 = us.TF_E = us.TF_H = 0.0;
-    if (tc.nl0 > 0.0) us.TF_L0 = pred_intf<UNIT, true>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L0, FG);
-    if (tc.nl1 > 0.0) us.TF_L1 = pred_intf<UNIT, true>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L1, FG);
+    if (tc.nl0 > 0.0) us.TF_L0 = pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L0, FG);
+    if (tc.nl1 > 0.0) us.TF_L1 = pred_intf<UNIT>(tc.L.C_F, tc.L.N_F, us.FH_L, us.FD_L1, FG);
     if (tc.first) {
         us.FH_E = kW * tc.E.sWh;
         us.FD_E = kA * tc.E.sAd;
-        us.TF_E = pred_intf<UNIT, true>(tc.E.C_F, tc.E.N_F, us.FH_E, us.FD_E, FG);
+        us.TF_E = pred_intf<UNIT>(tc.E.C_F, tc.E.N_F, us.FH_E, us.FD_E, FG);
     }
     if (tc.last) {
         us.FH_H = kW * tc.H.sWh;
         us.FD_H = kA * tc.H.sAd;
-        us.TF_H = pred_intf<UNIT, true>(tc.H.C_F, tc.H.N_F, us.FH_H, us.FD_H, FG);
+        us.TF_H = pred_intf<UNIT>(tc.H.C_F, tc.H.N_F, us.FH_H, us.FD_H, FG);
     }
 }
 
@@ -349,8 +334,8 @@ __device__ __noinline__ double block_backward(const BlockConst& b, bool r1, doub
     const double sAh = r1 ? b.sAh1 : b.sAh;
     const double CB = r1 ? b.C_B1 : b.C_B;                   // a checkpointed layer recomputes (L17)
     const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
-    const double TB = pred_intf<UNIT, true>(CB, b.N_B, BH, BD, FG);
-    dBp = (b.N_Bp == b.N_B) ? 0.0 : pred_intf<UNIT, true>(CB, b.N_Bp, BH, BD, FG) - TB;
+    const double TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, FG);
+    dBp = (b.N_Bp == b.N_B) ? 0.0 : pred_intf<UNIT>(CB, b.N_Bp, BH, BD, FG) - TB;
     return TB;
 }
 
@@ -411,8 +396,13 @@ __device__ __forceinline__ double d_kO(const TupleConst& tc, const UnitState& us
 // at least that long again, so T >= x_m + ov (1 - 1/F_m) for every m in S (and
 // T >= ov for the zero channels, which have g = 0 in the table).  Unit factors
 // make Alg. 1 the max itself, so only R4 is used there.
-__device__ MIST_LB_ATTR double lb_row_gen(double x0, double x1, double x2, double x3, const FGRow* FG);
+__device__ __forceinline__ double lb_row_gen(double x0, double x1, double x2, double x3, const FGRow* FG);
 
+// NI: one shared, called copy of the bound row instead of an inlined copy per call
+// site.  The eval kernel's SASS (~127 KB) is far above the 32 KB L1.5 instruction
+// cache; the called copy pays where the kO loops are short (Q = 10: cfg2 25.0 ->
+// 22.7 ms) and costs where they are long (Q = 50: cfg5 windows +1.5-3%), so the
+// launcher picks it by Q (eval_ni).
 __device__ __noinline__ double lb_row_ni(double x0, double x1, double x2, double x3, const FGRow* FG) {
     return lb_row_gen(x0, x1, x2, x3, FG);
 }
@@ -420,13 +410,11 @@ __device__ __noinline__ double lb_row_ni(double x0, double x1, double x2, double
 template <bool UNIT, bool NI = false>
 __device__ __forceinline__ double lb_row(double x0, double x1, double x2, double x3, const FGRow* FG) {
     if (UNIT) return dmax(dmax(x0, x1), dmax(x2, x3));
-#ifdef MIST_SEL_NI
     if (NI) return lb_row_ni(x0, x1, x2, x3, FG);
-#endif
     return lb_row_gen(x0, x1, x2, x3, FG);
 }
 
-__device__ MIST_LB_ATTR double lb_row_gen(double x0, double x1, double x2, double x3, const FGRow* FG) {
+__device__ __forceinline__ double lb_row_gen(double x0, double x1, double x2, double x3, const FGRow* FG) {
     const double mx = dmax(dmax(x0, x1), dmax(x2, x3));
     const unsigned pat = (unsigned)(x0 != 0.0) | ((unsigned)(x1 != 0.0) << 1) | ((unsigned)(x2 != 0.0) << 2) |
                          ((unsigned)(x3 != 0.0) << 3);
@@ -455,25 +443,25 @@ __device__ __forceinline__ bool fp_pattern_fixed(const TupleConst& tc, const Run
 
 // Lower bound of d at config kO: rs.dbase + sum count * (lb_row(F') - T(F)) over the blocks.
 // `scale` bounds the magnitudes summed, for a rounding margin.
-template <bool UNIT>
+template <bool UNIT, bool NI>
 __device__ MIST_DLB_ATTR double d_lower_bound(const TupleConst& tc, const UnitState& us, const RunState& rs,
                                                 double kO, const FGRow* FG, double& scale) {
     double lb = rs.dbase, sc = fabs(rs.dbase);
     const double H = rs.FpH_L + kO * tc.L.sOh;
     if (tc.nl0 > 0.0) {
-        const double m = lb_row<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, FG);
+        const double m = lb_row<UNIT, NI>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L0 + kO * tc.L.sOd, FG);
         lb += tc.nl0 * (m - us.TF_L0); sc += tc.nl0 * (m + us.TF_L0);
     }
     if (tc.nl1 > 0.0) {
-        const double m = lb_row<UNIT>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, FG);
+        const double m = lb_row<UNIT, NI>(tc.L.C_F, tc.L.N_Fp, H, rs.FpD_L1 + kO * tc.L.sOd, FG);
         lb += tc.nl1 * (m - us.TF_L1); sc += tc.nl1 * (m + us.TF_L1);
     }
     if (tc.first) {
-        const double m = lb_row<UNIT>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG);
+        const double m = lb_row<UNIT, NI>(tc.E.C_F, tc.E.N_Fp, rs.FpH_E + kO * tc.E.sOh, rs.FpD_E + kO * tc.E.sOd, FG);
         lb += m - us.TF_E; sc += m + us.TF_E;
     }
     if (tc.last) {
-        const double m = lb_row<UNIT>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG);
+        const double m = lb_row<UNIT, NI>(tc.H.C_F, tc.H.N_Fp, rs.FpH_H + kO * tc.H.sOh, rs.FpD_H + kO * tc.H.sOd, FG);
         lb += m - us.TF_H; sc += m + us.TF_H;
     }
     scale = sc;
@@ -486,24 +474,40 @@ __device__ MIST_DLB_ATTR double d_lower_bound(const TupleConst& tc, const UnitSt
 // D2H = kG sGd grow with kG, R5 is monotone in the channels while the nonzero
 // pattern is fixed (every kG >= 1), and R4 (the max, used at kG = 0) lies below R5
 // at kG = 1.  So the runs whose bound clears the staircase are a suffix in kG.
-template <bool UNIT>
+template <bool UNIT, bool NI>
 __device__ __forceinline__ double lb_backward(const BlockConst& b, bool r1, double FH, double kG, double kA,
                                               const FGRow* FG) {
     const double CB = r1 ? b.C_B1 : b.C_B;
     const double BH = FH + kG * b.sGh + kA * (r1 ? b.sAh1 : b.sAh), BD = kG * b.sGd;
     if (kG == 0.0) return dmax(dmax(CB, b.N_B), dmax(BH, BD));
-    return lb_row<UNIT, true>(CB, b.N_B, BH, BD, FG);
+    return lb_row<UNIT, NI>(CB, b.N_B, BH, BD, FG);
 }
 
-template <bool UNIT>
+template <bool UNIT, bool NI>
 __device__ __forceinline__ double run_t_lb(const TupleConst& tc, const UnitState& us, double kG, double kA,
                                            const FGRow* FG) {
     double tb = 0.0;
-    if (tc.nl0 > 0.0) tb += tc.nl0 * lb_backward<UNIT>(tc.L, false, us.FH_L, kG, kA, FG);
-    if (tc.nl1 > 0.0) tb += tc.nl1 * lb_backward<UNIT>(tc.L, true, us.FH_L, kG, kA, FG);
-    if (tc.first) tb += lb_backward<UNIT>(tc.E, false, us.FH_E, kG, kA, FG);
-    if (tc.last) tb += lb_backward<UNIT>(tc.H, false, us.FH_H, kG, kA, FG);
+    if (tc.nl0 > 0.0) tb += tc.nl0 * lb_backward<UNIT, NI>(tc.L, false, us.FH_L, kG, kA, FG);
+    if (tc.nl1 > 0.0) tb += tc.nl1 * lb_backward<UNIT, NI>(tc.L, true, us.FH_L, kG, kA, FG);
+    if (tc.first) tb += lb_backward<UNIT, NI>(tc.E, false, us.FH_E, kG, kA, FG);
+    if (tc.last) tb += lb_backward<UNIT, NI>(tc.H, false, us.FH_H, kG, kA, FG);
     return (unit_tf(tc, us) + tb) + tc.t_p2p;
+}
+
+// R7 for a whole tuple (ykey = d): every channel is non-decreasing in the ratio
+// indices (O6), so every config of the tuple has t >= sum count (R4(F at kW = kA =
+// 0) + R4(B at kG = kW = kA = 0)) + p2p = sum count (max(C_F, N_F) + max(C_B, N_B))
+// + p2p.  When the group's y = 0 staircase point lies strictly left of that, every
+// unit of the tuple is beaten (same argument as run_cut) and none is set up.
+__device__ __forceinline__ bool tuple_cut(const TupleConst& tc, const double* ft, const double* fy, long long lo,
+                                          long long hi) {
+    if (lo >= hi || !(fy[hi - 1] <= 0.0)) return false;
+    double tb = 0.0;
+    if (tc.nl0 > 0.0) tb += tc.nl0 * (dmax(tc.L.C_F, tc.L.N_F) + dmax(tc.L.C_B, tc.L.N_B));
+    if (tc.nl1 > 0.0) tb += tc.nl1 * (dmax(tc.L.C_F, tc.L.N_F) + dmax(tc.L.C_B1, tc.L.N_B));
+    if (tc.first) tb += dmax(tc.E.C_F, tc.E.N_F) + dmax(tc.E.C_B, tc.E.N_B);
+    if (tc.last) tb += dmax(tc.H.C_F, tc.H.N_F) + dmax(tc.H.C_B, tc.H.N_B);
+    return ft[hi - 1] < (tb + tc.t_p2p) * (1.0 - 1e-12);
 }
 
 // End of the runs of a unit that the pilot staircase cannot rule out: runs
@@ -514,7 +518,7 @@ __device__ __forceinline__ double run_t_lb(const TupleConst& tc, const UnitState
 // mem the unit's smallest mem is its (kG, kO) = (kmax, kmax) config exactly (O9
 // is non-increasing in kG and kO under the kG-suffix property, R2').  The t bound
 // carries a 1e-12 relative margin for the rounding of R4/R5 against Alg. 1.
-template <bool UNIT>
+template <bool UNIT, bool NI = false>
 __device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst& tc, const UnitState& us, unsigned kW, unsigned kA,
                             unsigned g0, unsigned gend, const FGRow* FG, const double* ft, const double* fy,
                             long long lo, long long hi, const unsigned* vals = nullptr) {
@@ -531,7 +535,7 @@ __device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst&
         return gend;                           // no y = 0 point: nothing below every d
     }
     auto cut = [&](unsigned g) -> bool {
-        const double lb = run_t_lb<UNIT>(tc, us, (double)(vals ? vals[g] : g), dkA, FG) * (1.0 - 1e-12);
+        const double lb = run_t_lb<UNIT, NI>(tc, us, (double)(vals ? vals[g] : g), dkA, FG) * (1.0 - 1e-12);
         if (!P.ykey) return ft[hi - 1] < lb;
         long long a = lo, b = hi;              // points with t < lb: [lo, a)
         while (a < b) {
@@ -637,7 +641,7 @@ struct FiltView {
     const int64_t* off;     // null: no filter
 };
 
-template <bool UNIT, int MODE>
+template <bool UNIT, int MODE, bool NI = false>
 __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalArgs& A, const TupleConst& tc,
                                                 const UnitState& us, unsigned kW, unsigned kG, unsigned kA,
                                                 unsigned radix, double Q, int Q1, unsigned grp, const FGRow* FG,
@@ -713,7 +717,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             const u64 idx = idx0 + (u64)ko * Q1;
             if (FILT && !P.ykey) {
                 double scale;
-                const double lb = d_lower_bound<UNIT>(tc, us, rs, kO, FG, scale);
+                const double lb = d_lower_bound<UNIT, NI>(tc, us, rs, kO, FG, scale);
                 const double thr = best_y < y_thr ? best_y : y_thr;
                 if (lb - 1e-12 * scale > thr) {
                     if (A.fp) continue;                       // keep counting feasible configs
@@ -796,7 +800,7 @@ k_eval(DevProblem P, EvalArgs A) {
         if (active) unit_forward<UNIT>(tc, dkW, dkA, FG, us);
         // R7 (frontier and pilot modes): runs ig >= icut are beaten by the staircase on t alone
         unsigned icut = radix;
-        if (MODE != 1 && active && A.f_off && !A.fp && !A.no_r7)
+        if (MODE != 1 && active && A.f_off && !A.fp && !(A.no_r7 & 1))
             icut = run_cut<UNIT>(P, tc, us, kW, kA, 0u, radix, FG, A.f_t, A.f_y, A.f_off[grp], A.f_off[grp + 1],
                                  MODE == 2 ? A.vals : nullptr);
         // phase rows evaluated by this thread (PredINTF calls), for the roofline's algorithmic count
@@ -907,7 +911,7 @@ k_eval(DevProblem P, EvalArgs A) {
 // window at about the same time (less time waiting at the window barrier).
 // UPW (CTA queue only): units per thread per window; a window of NT*UPW units
 // halves the window boundaries (and their barrier tails) for UPW = 2.
-template <bool UNIT, int NT, int MINB, bool CQ, int UPW>
+template <bool UNIT, int NT, int MINB, bool CQ, int UPW, bool NI = false>
 __global__ void __launch_bounds__(NT, MINB)
 k_eval_q(DevProblem P, EvalArgs A) {
     static_assert(CQ || UPW == 1, "several units per thread need the CTA queue");
@@ -990,7 +994,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
         }
         FiltView fv;
         fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
-        const bool r7 = fv.off != nullptr && A.fp == nullptr && A.no_r7 == 0;
+        const bool r7 = fv.off != nullptr && A.fp == nullptr && !(A.no_r7 & 1);
         unsigned total = 0;
         // per-thread state of unit j = 0 (the warp queue of the non-CQ path reads it)
         unsigned tk = 0, kW = 0, kA = 0, g0 = radix, excl = 0;
@@ -1001,8 +1005,13 @@ k_eval_q(DevProblem P, EvalArgs A) {
             const unsigned tkj = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
             const unsigned jj = (unsigned)(u - (tb0 + tkj) * (u64)upt);
             const unsigned kWj = jj / radix, kAj = jj - kWj * radix;
-            const bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
-                                kAj <= (unsigned)P.kmax[3];              // preset ranges
+            bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
+                          kAj <= (unsigned)P.kmax[3];                    // preset ranges
+            if (active && r7 && !P.ykey && !(A.no_r7 & 2) && tuple_cut(sT[tkj], fv.t, fv.y, fv.off[sT[tkj].group],
+                                                     fv.off[sT[tkj].group + 1])) {
+                active = false;
+                MIST_CTR(4, (unsigned)P.kmax[1] + 1u);
+            }
             const unsigned gend = (unsigned)P.kmax[1] + 1u;              // runs kG < gend
             unsigned g0j = radix, g1j = gend;
             {
@@ -1023,7 +1032,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                     // R7: runs the staircase beats on t alone are never dealt (not with
                     // fingerprints, which count every feasible config)
                     if (r7 && g0j < gend) {
-                        g1j = run_cut<UNIT>(P, tc, us, kWj, kAj, g0j, gend, FG, fv.t, fv.y, fv.off[tc.group],
+                        g1j = run_cut<UNIT, NI>(P, tc, us, kWj, kAj, g0j, gend, FG, fv.t, fv.y, fv.off[tc.group],
                                             fv.off[tc.group + 1]);
                         MIST_CTR(4, gend - g1j);
                     }
@@ -1115,7 +1124,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                 const unsigned brows = nrows * (tc.L.N_Bp != tc.L.N_B ? 2u : 1u);
                 const bool same = cv && cgrp == grp;
                 u64 fcnt = 0, fhash = 0;
-                const RunCand rc = frontier_run<UNIT, 0>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
+                const RunCand rc = frontier_run<UNIT, 0, NI>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
                                                          ct, cy, nrows, brows, nph, fcnt, fhash, fv, ctr);
                 if (A.fp && fcnt) {
                     atomicAdd(A.fp + 2 * (u64)grp, fcnt);
@@ -1336,7 +1345,7 @@ static int eval_cfg() {
     return v;
 }
 
-template <bool UNIT, int NT, int MINB, bool CQ, int UPW = 1>
+template <bool UNIT, int NT, int MINB, bool CQ, int UPW = 1, bool NI = false>
 static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     constexpr size_t NW = (size_t)NT * UPW;
     const size_t maxt = (NW + A.upt - 1) / A.upt + 1;
@@ -1346,19 +1355,19 @@ static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& 
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static std::atomic<unsigned long long> attr_set{0};   // the attribute is per device: one bit per device
     if (device >= 64 || !((attr_set.load() >> device) & 1ull)) {
-        cudaError_t e = cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ, UPW>,
+        cudaError_t e = cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ, UPW, NI>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
         if (device < 64) attr_set.fetch_or(1ull << device);
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW, NI>, NT, smem);
     if (per_sm < 1) per_sm = 1;
     u64 blocks = (A.n_units + NW - 1) / NW;
     const u64 cap = (u64)sm_count(device) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) return cudaSuccess;
-    k_eval_q<UNIT, NT, MINB, CQ, UPW><<<(unsigned)blocks, NT, smem, st>>>(P, A);
+    k_eval_q<UNIT, NT, MINB, CQ, UPW, NI><<<(unsigned)blocks, NT, smem, st>>>(P, A);
     return cudaGetLastError();
 }
 
@@ -1384,10 +1393,23 @@ static int eval_queue() {
     return v;
 }
 
+// Called (not inlined) bound rows in the frontier kernel unless the kO loops are long:
+// Q < 40 by default (measured same-box: cfg4 Q = 8 274 -> 263 ms, cfg2 Q = 10 25.0 ->
+// 22.7 ms, cfg3 Q = 20 166 -> 153 ms; cfg5 Q = 50 windows 1.5-3% slower,
+// profiles/r2/ab_noinline_summary.txt, ab_chunk_summary.txt); MIST_EVAL_NI=0/1 forces.
+static bool eval_ni(int Q) {
+    const char* s = getenv("MIST_EVAL_NI");
+    if (s && (s[0] == '0' || s[0] == '1')) return s[0] == '1';
+    return Q < 40;
+}
+
 template <bool UNIT>
 static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     if (eval_queue() == 2) {
-        if (eval_upw() == 2) return launch_eval_q<UNIT, 256, 2, true, 2>(st, device, P, A);
+        if (eval_upw() == 2) {
+            if (!UNIT && eval_ni(P.Q)) return launch_eval_q<UNIT, 256, 2, true, 2, true>(st, device, P, A);
+            return launch_eval_q<UNIT, 256, 2, true, 2>(st, device, P, A);
+        }
         switch (eval_cfg()) {
             case 0: return launch_eval_q<UNIT, 256, 2, true>(st, device, P, A);
             default: return launch_eval_q<UNIT, 256, 3, true>(st, device, P, A);

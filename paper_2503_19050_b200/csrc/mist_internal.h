@@ -121,7 +121,7 @@ struct EvalArgs {
     const double* f_y;
     const unsigned long long* f_idx;
     const int64_t* f_off;       // [n_groups+1], null = no filter
-    int no_r7;                  // 1: no run cut before the backward rows (A/B knob MIST_R7=0)
+    int no_r7;                  // A/B knob: bit 0 no R7 at all (MIST_R7=0), bit 1 no tuple-level cut (MIST_R7=unit)
 };
 
 struct ReduceStats {
