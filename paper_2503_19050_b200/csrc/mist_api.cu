@@ -545,6 +545,7 @@ struct SweepCtx {
     long long C = 0, count = 0;
     bool filter = false;
     bool want_fp = false;
+    u64 twin_floor = ~0ull;       // L20 twins at or above this tuple are skipped (~0: none)
 };
 
 static mist_status_t read_count(mist_ctx_t* ctx, SweepCtx& S, long long* out) {
@@ -610,6 +611,7 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     A.cand = ctx->cand;
     A.cand_count = S.d_count;
     A.fp = mode == 0 ? S.d_fp : nullptr;
+    A.twin_floor = (mode == 0 && S.d_fp) ? ~0ull : S.twin_floor;   // fingerprints count every feasible config
     A.phases = mode == 0 ? S.d_phases : nullptr;
     A.nv = nv;
     for (unsigned i = 0; i < nv && i < 16; ++i) A.vals[i] = vals[i];
@@ -655,13 +657,17 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
 }
 
 static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vector<std::pair<u64, u64>>& ranges,
-                           bool want_fp, long long* n_front) {
+                           bool want_fp, u64 twin_floor, long long* n_front) {
     u64 n_tuples = 0;
     for (auto& r : ranges) n_tuples += r.second - r.first;
     const u64 total_runs = n_tuples * pp.R3;
     SweepCtx S;
     S.pp = &pp;
     S.want_fp = want_fp;
+    {
+        const char* e = getenv("MIST_DEDUP");
+        S.twin_floor = (e && e[0] == '0') ? ~0ull : twin_floor;
+    }
     // candidate capacity: 2^26 records (2.4 GB + 1 GB sort scratch), less for small ranges
     S.C = std::min<long long>(1LL << 26, next_pow2((long long)std::min<u64>(total_runs, 1ull << 40) * 2 + 4096));
     mist_status_t st = ensure_cand(ctx, S.C);
@@ -766,6 +772,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
                 A.n_units = b - a;
                 A.cand = ctx->cand;
                 A.cand_count = S.d_count;
+                A.twin_floor = S.twin_floor;
                 const int hz = ev_begin(ctx, CAT_PILOT);
                 CK(launch_pilot_zero(ctx->stream, ctx->device, pp.P, A), "pilot zero");
                 ev_end(ctx, hz);
@@ -889,7 +896,9 @@ static mist_status_t frontier_device(mist_ctx_t* ctx, const Prepared& pp, uint64
     for (auto& r : ranges) mine += r.second - r.first;
     long long nf = 0;
     if (mine > 0) {
-        st = sweep(ctx, pp, ranges, want_fp, &nf);
+        // L20 twins: the whole space (t_end == 0, all ranks together) holds every twin;
+        // an explicit range holds the twins at or above its first tuple
+        st = sweep(ctx, pp, ranges, want_fp, t_end == 0 ? 0ull : tb, &nf);
         if (st != MIST_OK) return st;
     } else {
         CK(ensure(ctx->fp, sizeof(u64) * 2 * (size_t)pp.ng), "alloc fp");

@@ -81,7 +81,8 @@ __device__ void make_tuple(const DevProblem& P, const DevGroup* groups, int ng,
     const u64 per_split = (u64)P.nz * (G.l + 1);
     const int split = (int)(local / per_split);
     const int rem = (int)(local - (u64)split * per_split);
-    const int z = P.zlev[rem / (G.l + 1)];
+    const int zi = rem / (G.l + 1);
+    const int z = P.zlev[zi];
     const int c = rem % (G.l + 1);
     const int TP = G.tp[split], DP = G.dp[split], b = G.b[split], ti = G.ti[split];
     const int rows = P.n_b * P.n_tp;
@@ -140,6 +141,8 @@ __device__ void make_tuple(const DevProblem& P, const DevGroup* groups, int ng,
     // preset: CKPT c in {0, l} only -- a tuple outside it is
     // never feasible (every D*mem >= 0 > -1)
     if (P.ckpt_ends && c != 0 && c != l) o.DMB = -1.0;
+    o.twin_T = (DP == 1 && zi > 0) ? T - (u64)zi * (u64)(l + 1) : ~0ull;
+    o.pad_ = 0;
 }
 
 // a2 over a rank's block-cyclic share: seg[2*s] = first tuple of segment s,
@@ -792,7 +795,8 @@ k_eval(DevProblem P, EvalArgs A) {
         // preset: a unit with kW or kA beyond its ratio's range has no configuration in
         // the space (the dense mode still writes t, d, mem for it, with feasible = 0)
         const bool in_unit = kW <= (unsigned)P.kmax[0] && kA <= (unsigned)P.kmax[3];
-        const bool active = unit_ok && (MODE == 1 || in_unit);
+        const bool twin = MODE != 1 && unit_ok && sT[tk].twin_T != ~0ull && sT[tk].twin_T >= A.twin_floor;
+        const bool active = unit_ok && (MODE == 1 || in_unit) && !twin;
         const double dkW = kW, dkA = kA;
         const TupleConst& tc = sT[tk];
         const unsigned grp = tc.group;
@@ -1007,6 +1011,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
             const unsigned kWj = jj / radix, kAj = jj - kWj * radix;
             bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
                           kAj <= (unsigned)P.kmax[3];                    // preset ranges
+            if (active && sT[tkj].twin_T >= A.twin_floor && sT[tkj].twin_T != ~0ull) active = false;   // L20 twin
             if (active && r7 && !P.ykey && !(A.no_r7 & 2) && tuple_cut(sT[tkj], fv.t, fv.y, fv.off[sT[tkj].group],
                                                      fv.off[sT[tkj].group + 1])) {
                 active = false;
@@ -1188,7 +1193,8 @@ k_pilot_zero(DevProblem P, EvalArgs A) {
                                (!tc.last || tc.H.N_Bp == tc.H.N_B);
             const bool fp_eq = tc.L.N_Fp == tc.L.N_F && (!tc.first || tc.E.N_Fp == tc.E.N_F) &&
                                (!tc.last || tc.H.N_Fp == tc.H.N_F);
-            if (bp_eq && fp_eq && !(tc.DMB < 0.0)) {
+            const bool twin = tc.twin_T != ~0ull && tc.twin_T >= A.twin_floor;
+            if (bp_eq && fp_eq && !(tc.DMB < 0.0) && !twin) {
                 for (int kA = 0; kA <= P.kmax[3]; ++kA) {
                     RunState rs;
                     run_memory(tc, 0.0, 0.0, (double)kA, Q, rs);

@@ -75,6 +75,13 @@ struct TupleConst {
     double DA, DAx;                // D*A_full, [c>0]*D*A_full
     double DMB;                    // D*Mem_Budget
     double D;
+    // L20 twin: at DP = 1 every ZeRO level has the same t and d (all sigmas 1, no DP
+    // collective) and a memory non-decreasing in z, so a tuple with z above the lowest
+    // enumerated level is beaten config by config by its twin at the lowest level
+    // (same group, split and c; smaller idx).  twin_T = that twin's global tuple
+    // index, or ~0 when the tuple is not such a duplicate.
+    unsigned long long twin_T;
+    unsigned long long pad_;
 };
 
 // Candidate buffer (SoA).  One record per kept OO-run (P13 prefilter).
@@ -122,6 +129,9 @@ struct EvalArgs {
     const unsigned long long* f_idx;
     const int64_t* f_off;       // [n_groups+1], null = no filter
     int no_r7;                  // A/B knob: bit 0 no R7 at all (MIST_R7=0), bit 1 no tuple-level cut (MIST_R7=unit)
+    // L20 twins: a tuple with twin_T >= twin_floor is skipped (its twin is swept in
+    // the same call); ~0 disables (fingerprints, MIST_DEDUP=0)
+    unsigned long long twin_floor;
 };
 
 struct ReduceStats {

@@ -183,3 +183,45 @@ def test_sampling():
         assert a in mine.tolist()        # alpha = 1: minimum t
     with pytest.raises(ValueError):
         o.sample(res["points"], res["offsets"], K=1)
+
+
+def test_dp1_zero_level_twins():
+    """L20 (DESIGN R9): at DP = 1 all sigmas are 1 and every DP collective is 0
+    (O4-O6), so the ZeRO levels of a tuple share t and d exactly while mem is
+    non-decreasing in z (O9: z = 3 adds the gathered layers, z >= 2 the
+    unsharded grads).  Hence every z above the lowest level is beaten by its
+    lowest-level twin (smaller idx), and no frontier point of the oracle has
+    DP = 1 and z above the lowest enumerated level."""
+    for seed, pb in enumerate([tiny(4, 4, 1, 4, 8, 2), tiny(3, 4, 2, 2, 8, 2, factors="spec"),
+                               tiny(5, 4, 2, 4, 12, 2, kv_heads=2, g=1, p=1), random_problem(3)]):
+        try:
+            o = Oracle(pb)
+        except ValueError:
+            continue
+        Q1 = pb.Q + 1
+        rng = np.random.default_rng(seed)
+        seen = 0
+        for gi, g in enumerate(o.groups):
+            for sp in range(g.n_splits):
+                if g.dp[sp] != 1:
+                    continue
+                for _ in range(6):
+                    c = int(rng.integers(0, g.l + 1))
+                    k = [int(v) for v in rng.integers(0, Q1, 4)]
+                    base = o.detail(gi, sp, 0, c, *k)
+                    for z in (1, 2, 3):
+                        d = o.detail(gi, sp, z, c, *k)
+                        assert d.t == base.t and d.d == base.d
+                        assert d.mem >= base.mem
+                        seen += 1
+        if o.n_configs <= 300_000:
+            res = o.sweep(ykey=0, threads=2)
+            R = Q1 ** 4
+            for g in range(o.n_groups):
+                G = o.groups[g]
+                for p in res["points"][res["offsets"][g]:res["offsets"][g + 1]]:
+                    local = int(p["idx"]) // R - int(G.config_offset) // R
+                    per_split = 4 * (G.l + 1)
+                    sp, z = local // per_split, (local % per_split) // (G.l + 1)
+                    assert not (G.dp[sp] == 1 and z > 0)
+        assert seen > 0 or seed == 3
