@@ -364,6 +364,9 @@ extern "C" void mist_ctx_destroy(mist_ctx_t* ctx) {
         release(*b);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    ctx->cache_points.release();
+    ctx->cache_offsets.release();
+    ctx->cache_fp.release();
     delete ctx;
 }
 
@@ -983,15 +986,15 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         ev_end(ctx, htot);
         ctx->stats.d2h_bytes = sizeof(mist_point_t) * (uint64_t)nf + sizeof(int64_t) * ((uint64_t)pp.ng + 1) +
                                (want_fp ? sizeof(u64) * 2 * (uint64_t)pp.ng : 0);
-        ctx->cache_points.resize((size_t)nf);
-        ctx->cache_offsets.resize((size_t)pp.ng + 1);
+        CK(ctx->cache_points.resize((size_t)nf), "pinned points");
+        CK(ctx->cache_offsets.resize((size_t)pp.ng + 1), "pinned offsets");
         if (nf > 0)
             CK(cudaMemcpyAsync(ctx->cache_points.data(), d_pts, sizeof(mist_point_t) * (size_t)nf,
                                cudaMemcpyDeviceToHost, ctx->stream), "D2H points");
         CK(cudaMemcpyAsync(ctx->cache_offsets.data(), d_off, sizeof(int64_t) * ((size_t)pp.ng + 1),
                            cudaMemcpyDeviceToHost, ctx->stream), "D2H offsets");
         if (want_fp) {
-            ctx->cache_fp.resize(2 * (size_t)pp.ng);
+            CK(ctx->cache_fp.resize(2 * (size_t)pp.ng), "pinned fp");
             CK(cudaMemcpyAsync(ctx->cache_fp.data(), ctx->fp.p, sizeof(u64) * 2 * (size_t)pp.ng,
                                cudaMemcpyDeviceToHost, ctx->stream), "D2H fp");
         }

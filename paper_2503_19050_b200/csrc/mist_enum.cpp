@@ -174,27 +174,47 @@ extern "C" mist_status_t mist_enumerate_space(const mist_model_t* model, int64_t
             }
         }
 
-    // keys (G, first, last, w, l, n, m)
+    // keys (G, first, last, w, l, n, m), deduplicated, in lexicographic order.  Stage i
+    // of S matters only through its context (first = [i = 1], last = [i = S], w =
+    // min(G, S - i + 1)), and for S >= 2 it admits l = 1 .. L - S + 1, so per G the
+    // key set is: for every (context, shape) the l range of the smallest valid S,
+    // plus the single-stage key (l = L on the full mesh).  Generated directly in
+    // sorted order (no sort of the per-(S, i, l) candidates).
     std::vector<std::array<int, 7>> keys;
-    for (int G : Gs)
-        for (int S = 1; S <= S_max; ++S) {
-            // stage i only matters through (first, last, w); enumerate distinct contexts
-            for (int i = 1; i <= S; ++i) {
-                const int first = i == 1, last = i == S, w = std::min(G, S - i + 1);
-                for (auto& sh : shapes) {
-                    const int rest = devices - sh[0] * sh[1];
-                    if (rest < 0 || !reach[S - 1][rest]) continue;
-                    if (S == 1) {
-                        keys.push_back({G, first, last, w, L, sh[0], sh[1]});
-                    } else {
-                        for (int l = 1; l <= L - (S - 1); ++l)
-                            keys.push_back({G, first, last, w, l, sh[0], sh[1]});
-                    }
-                }
+    const int nsh = (int)shapes.size();   // sorted by (n, m): (1, 2^j) ascending, then (n >= 2, M)
+    const int W = S_max + 1;
+    std::vector<int> ml((size_t)4 * W * nsh);
+    std::vector<uint8_t> single((size_t)nsh);
+    auto at = [&](int first, int last, int w, int sh) -> int& {
+        return ml[(((size_t)(first * 2 + last) * W + w) * nsh) + sh];
+    };
+    for (int G : Gs) {
+        std::fill(ml.begin(), ml.end(), 0);
+        std::fill(single.begin(), single.end(), 0);
+        for (int S = 1; S <= S_max; ++S)
+            for (int sh = 0; sh < nsh; ++sh) {
+                const int rest = devices - shapes[sh][0] * shapes[sh][1];
+                if (rest < 0 || !reach[S - 1][rest]) continue;
+                if (S == 1) { single[sh] = 1; continue; }
+                const int lmax = L - S + 1;
+                auto upd = [&](int first, int last, int w) {
+                    int& v = at(first, last, w, sh);
+                    if (lmax > v) v = lmax;
+                };
+                upd(1, 0, std::min(G, S));                                   // i = 1
+                upd(0, 1, 1);                                                // i = S
+                for (int v = 2; v <= S - 1; ++v) upd(0, 0, std::min(G, v));  // 1 < i < S
             }
-        }
-    std::sort(keys.begin(), keys.end());
-    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        for (int first = 0; first <= 1; ++first)
+            for (int last = 0; last <= 1; ++last)
+                for (int w = 1; w <= S_max; ++w)
+                    for (int l = 1; l <= L; ++l)
+                        for (int sh = 0; sh < nsh; ++sh) {
+                            const bool ok = (first && last) ? (single[sh] && w == 1 && l == L)
+                                                            : l <= at(first, last, w, sh);
+                            if (ok) keys.push_back({G, first, last, w, l, shapes[sh][0], shapes[sh][1]});
+                        }
+    }
 
     int nz = 0;
     for (int z = 0; z < 4; ++z) nz += space->zero_mask >> z & 1;

@@ -295,6 +295,34 @@ __device__ __forceinline__ unsigned first_feasible_kO(const TupleConst& tc, cons
     return (unsigned)k;
 }
 
+// First run (kG) of a unit whose kO = kOend config fits the budget, in closed form
+// (R2' applied to kG, like R2" to kO): under the kG-suffix property (mG >= gb_k),
+// D*Mem_fwd and D*Mem_bwd at kO = kOend are affine in kG with slopes -mG and
+// -(mG - gb_k), so the boundary is the max of two ceilings; a float reciprocal
+// under-estimates it and the exact integer test walks up to it.  Returns gend when
+// no run of the unit is feasible.
+__device__ __forceinline__ unsigned first_feasible_kG(const TupleConst& tc, double kW, double kA, unsigned gend,
+                                                      double kOend, double Q) {
+    RunState r0;
+    run_memory(tc, kW, 0.0, kA, Q, r0);
+    const double f0 = r0.Kf + tc.mO * (Q - kOend) + tc.ob_k * kOend;
+    const double b0 = r0.Kb + tc.mO * (Q - kOend);
+    if (dmax(f0, b0) <= tc.DMB) return 0u;
+    const double sb = tc.mG - tc.gb_k;
+    double g = 0.0;
+    if (f0 > tc.DMB) g = tc.mG > 0.0 ? (f0 - tc.DMB) * (double)__frcp_rn((float)tc.mG) : 1e30;
+    if (b0 > tc.DMB) g = dmax(g, sb > 0.0 ? (b0 - tc.DMB) * (double)__frcp_rn((float)sb) : 1e30);
+    g = g * (1.0 - 1e-5) - 1e-5;                           // under-estimate (float reciprocal: 2^-23 relative)
+    unsigned k = g > 1.0 ? (unsigned)ceil(g < (double)gend ? g : (double)gend) : 1u;
+    RunState rm;
+    while (k < gend) {
+        run_memory(tc, kW, (double)k, kA, Q, rm);
+        if (mem_kO(tc, rm, kOend, Q) <= tc.DMB) break;
+        ++k;
+    }
+    return k;
+}
+
 // F phases of the unit
 template <bool UNIT>
 __device__ __forceinline__ void unit_forward(const TupleConst& tc, double kW, double kA, const FGRow* FG,
@@ -1027,13 +1055,21 @@ k_eval_q(DevProblem P, EvalArgs A) {
                     sU[w] = us;
                     nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
                            (unsigned)(tc.last != 0);
-                    RunState rm;
-                    const double kOend = (double)P.kmax[2];
-                    for (unsigned ig = 0; ig < gend; ++ig) {
-                        run_memory(tc, (double)kWj, (double)ig, (double)kAj, Q, rm);
-                        if (mem_kO(tc, rm, kOend, Q) <= tc.DMB) { g0j = ig; break; }
+                    if (tc.mG >= tc.gb_k) {
+#ifdef MIST_G0_SCAN
+                        RunState rm;
+                        for (unsigned ig = 0; ig < gend; ++ig) {
+                            run_memory(tc, (double)kWj, (double)ig, (double)kAj, Q, rm);
+                            if (mem_kO(tc, rm, (double)P.kmax[2], Q) <= tc.DMB) { g0j = ig; break; }
+                        }
+#else
+                        const unsigned f = first_feasible_kG(tc, (double)kWj, (double)kAj, gend,
+                                                             (double)P.kmax[2], Q);
+                        g0j = f < gend ? f : radix;
+#endif
+                    } else {
+                        g0j = 0;                       // no kG-suffix property: every run is a task
                     }
-                    if (!(tc.mG >= tc.gb_k)) g0j = 0;  // no kG-suffix property: every run is a task
                     // R7: runs the staircase beats on t alone are never dealt (not with
                     // fingerprints, which count every feasible config)
                     if (r7 && g0j < gend) {
@@ -1413,6 +1449,10 @@ template <bool UNIT>
 static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     if (eval_queue() == 2) {
         if (eval_upw() == 2) {
+            if (eval_cfg() == 1) {   // A/B: 3 CTAs per SM (85 registers)
+                if (!UNIT && eval_ni(P.Q)) return launch_eval_q<UNIT, 256, 3, true, 2, true>(st, device, P, A);
+                return launch_eval_q<UNIT, 256, 3, true, 2>(st, device, P, A);
+            }
             if (!UNIT && eval_ni(P.Q)) return launch_eval_q<UNIT, 256, 2, true, 2, true>(st, device, P, A);
             return launch_eval_q<UNIT, 256, 2, true, 2>(st, device, P, A);
         }

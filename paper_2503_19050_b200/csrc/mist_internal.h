@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -145,6 +146,36 @@ struct ReduceStats {
 std::vector<std::pair<uint64_t, uint64_t>> mist_shard_blocks(uint64_t n_tuples, int rank, int world);
 
 namespace mist {
+// Host buffer in page-locked memory (D2H at full PCIe speed), grown on demand.
+// resize() keeps no contents; release() frees it.
+template <typename T>
+struct PinnedVec {
+    T* p = nullptr;
+    size_t n = 0, cap = 0;
+    cudaError_t resize(size_t m) {
+        if (m > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            const size_t want = std::max<size_t>(m, 1024);
+            cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&p), want * sizeof(T));
+            if (e != cudaSuccess) { p = nullptr; n = 0; return e; }
+            cap = want;
+        }
+        n = m;
+        return cudaSuccess;
+    }
+    T* data() { return p; }
+    const T* data() const { return p; }
+    size_t size() const { return n; }
+    T& operator[](size_t i) { return p[i]; }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = cap = 0;
+    }
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -164,10 +195,10 @@ struct mist_ctx {
     mist::DevBuf seg;   // scratch of the group-bucket frontier reduction (mist_segfront.cu)
     mist::CandBuf cand;            // views into cand_mem
     mist::SortScratch sort;        // views into sort_mem
-    // cached last frontier (for BUFFER_TOO_SMALL retries)
-    std::vector<mist_point_t> cache_points;
-    std::vector<int64_t> cache_offsets;
-    std::vector<uint64_t> cache_fp;
+    // cached last frontier (for BUFFER_TOO_SMALL retries), page-locked
+    mist::PinnedVec<mist_point_t> cache_points;
+    mist::PinnedVec<int64_t> cache_offsets;
+    mist::PinnedVec<uint64_t> cache_fp;
     uint64_t cache_key = 0;
     int cache_valid = 0;
     // timing events (pairs)

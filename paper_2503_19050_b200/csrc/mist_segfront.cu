@@ -37,8 +37,11 @@ typedef unsigned u32;
 cudaError_t scan_u32_exclusive(cudaStream_t st, const u32* in, u32* out, long long n, u32* tmp, u32* grand_total);
 long long scan_tmp_words(long long n);
 
-constexpr int kChunk = 2048;          // records per chunk (one CTA)
-constexpr int kChunkThreads = 256;
+#ifndef MIST_CHUNK
+#define MIST_CHUNK 1024
+#endif
+constexpr int kChunk = MIST_CHUNK;    // records per chunk (one CTA)
+constexpr int kChunkThreads = kChunk / 8;
 constexpr int kPerThread = kChunk / kChunkThreads;
 constexpr int kChunkSmem = (kChunk + 1) * (8 + 8 + 8) + kChunk * 2;   // t, y, idx (+ sentinel), permutation
 
@@ -319,35 +322,36 @@ cudaError_t frontier_reduce_seg(cudaStream_t st, CandBuf cand, long long n, int 
             if (d < 64) attr.fetch_or(1ull << d);
         }
     }
+    long long n_cur = n;                          // records entering the level (an upper bound)
     for (int level = 0;; ++level) {
         // a group whose frontier alone exceeds a chunk never fits one: give up after a few
         // levels and let the caller take the radix-sort path (same result)
         if (level == 8) return cudaErrorNotSupported;
+        // one host round trip per level: grids are sized from the bound n_cur / kChunk + ng on
+        // chunks (the kernels read the true count from the device), and the multi flag and the
+        // frontier total come back together at the end of the level
+        const long long nch_bound = n_cur / kChunk + ng + 1;
         err = cudaMemsetAsync(dev, 0, sizeof(u32) * 4, st);
+        if (err != cudaSuccess) return err;
+        err = cudaMemsetAsync(nf, 0, sizeof(u32) * (size_t)(nch_bound + 1), st);
         if (err != cudaSuccess) return err;
         k_seg_chunks<<<grid_n(ng, T), T, 0, st>>>(cnt, ng, cpg, dev + 1);
         err = scan_u32_exclusive(st, cpg, co, ng + 1, stmp, dev);    // co[ng] = chunks, dev[0] = chunks
         if (err != cudaSuccess) return err;
-        u32 h[2] = {0, 0};
+        const unsigned grid = (unsigned)std::min<long long>(nch_bound, cta);
+        k_chunk_front<<<grid, kChunkThreads, kChunkSmem, st>>>(X, cnt, goff, co, ng, dev, nf);
+        err = scan_u32_exclusive(st, nf, out, nch_bound + 1, stmp, dev + 2);
+        if (err != cudaSuccess) return err;
+        k_chunk_compact<<<grid, 128, 0, st>>>(X, goff, co, ng, dev, nf, out, Y);
+        rs->launches += 8;
+        rs->passes++;
+        u32 h[3] = {0, 0, 0};
         err = cudaMemcpyAsync(h, dev, sizeof(h), cudaMemcpyDeviceToHost, st);
         if (err != cudaSuccess) return err;
         err = cudaStreamSynchronize(st);
         if (err != cudaSuccess) return err;
-        const u32 nchunks = h[0];
-        k_chunk_front<<<std::min<u32>(std::max<u32>(nchunks, 1u), cta), kChunkThreads, kChunkSmem, st>>>(
-            X, cnt, goff, co, ng, dev, nf);
-        err = scan_u32_exclusive(st, nf, out, (long long)nchunks + 1, stmp, dev + 2);
-        if (err != cudaSuccess) return err;
-        k_chunk_compact<<<std::min<u32>(std::max<u32>(nchunks, 1u), cta), 128, 0, st>>>(X, goff, co, ng, dev, nf, out,
-                                                                                        Y);
-        rs->launches += 6;
-        rs->passes++;
         if (!h[1]) {                              // every group fitted one chunk: Y holds the frontier
-            u32 tot = 0;
-            err = cudaMemcpyAsync(&tot, dev + 2, sizeof(u32), cudaMemcpyDeviceToHost, st);
-            if (err != cudaSuccess) return err;
-            err = cudaStreamSynchronize(st);
-            if (err != cudaSuccess) return err;
+            const u32 tot = h[2];
             if (Y.t != A.t) {
                 k_seg_copy<<<grid_n(tot, T), T, 0, st>>>(Y, tot, A);
                 rs->launches++;
@@ -357,6 +361,7 @@ cudaError_t frontier_reduce_seg(cudaStream_t st, CandBuf cand, long long n, int 
         }
         k_seg_regroup<<<grid_n(ng, T), T, 0, st>>>(co, ng, out, cnt, goff);
         rs->launches++;
+        n_cur = h[2];
         std::swap(X, Y);
     }
 }
