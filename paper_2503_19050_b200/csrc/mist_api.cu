@@ -584,7 +584,7 @@ static mist_status_t reduce_buffer(mist_ctx_t* ctx, SweepCtx& S) {
 // If the candidates could overflow C/2, roll back (counter and fingerprints)
 // and split the range in halves, reducing in between.
 static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const TupleConst* tuples, u64 t_lo,
-                              u64 t_hi, unsigned nv, const unsigned* vals) {
+                              u64 t_hi, unsigned nv, const unsigned* vals, int unit_pass = 0) {
     const Prepared& pp = *S.pp;
     const unsigned radix = mode == 2 ? nv : (unsigned)pp.P.Q1;
     const unsigned R3 = radix * radix * radix;
@@ -598,7 +598,7 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
         // no staircase filter: emissions can approach one per run, so do not speculate
         const u64 piece = std::max<u64>(1, (u64)(S.C / 4) / R3);
         for (u64 a = t_lo; a < t_hi; a += piece) {
-            mist_status_t st = eval_opt(ctx, S, mode, tuples, a, std::min<u64>(t_hi, a + piece), nv, vals);
+            mist_status_t st = eval_opt(ctx, S, mode, tuples, a, std::min<u64>(t_hi, a + piece), nv, vals, unit_pass);
             if (st != MIST_OK) return st;
         }
         return MIST_OK;
@@ -617,6 +617,7 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     A.twin_floor = (mode == 0 && S.d_fp) ? ~0ull : S.twin_floor;   // fingerprints count every feasible config
     A.phases = mode == 0 ? S.d_phases : nullptr;
     A.nv = nv;
+    A.unit_pass = unit_pass;
     for (unsigned i = 0; i < nv && i < 16; ++i) A.vals[i] = vals[i];
     {
         const char* e = getenv("MIST_R7");
@@ -653,7 +654,7 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     u64 piece = (u64)std::max(1.0, room / std::max(per_tuple, 1e-9) * 0.5);
     piece = std::min<u64>(piece, (t_hi - t_lo + 1) / 2);
     for (u64 a = t_lo; a < t_hi; a += piece) {
-        st = eval_opt(ctx, S, mode, tuples, a, std::min<u64>(t_hi, a + piece), nv, vals);
+        st = eval_opt(ctx, S, mode, tuples, a, std::min<u64>(t_hi, a + piece), nv, vals, unit_pass);
         if (st != MIST_OK) return st;
     }
     return MIST_OK;
@@ -729,6 +730,8 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
         }
     }
     for (auto& nv : levels) nv = std::min(nv, Q + 1);
+    const char* penv = getenv("MIST_PASSES");
+    const int passes = (penv && penv[0] == '2') ? 2 : 1;
     const char* zenv = getenv("MIST_PILOT_ZERO");
     const bool zero_pilot = !(zenv && zenv[0] == '0');
     const char* env = getenv("MIST_PILOT");
@@ -808,7 +811,18 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
                 ctx->stats.pilot_configs += nT * (u64)nv * nv * nv * nv;
             }
         }
-        st = eval_opt(ctx, S, 0, tup, 0, nT, 0, nullptr);
+        if (passes == 2) {
+            // pass 1 (units with kW, kA even) refines the staircase that pass 2 filters with
+            st = eval_opt(ctx, S, 0, tup, 0, nT, 0, nullptr, 1);
+            if (st != MIST_OK) return st;
+            if (S.count > 0) {
+                st = reduce_buffer(ctx, S);
+                if (st != MIST_OK) return st;
+            }
+            st = eval_opt(ctx, S, 0, tup, 0, nT, 0, nullptr, 2);
+        } else {
+            st = eval_opt(ctx, S, 0, tup, 0, nT, 0, nullptr);
+        }
         if (st != MIST_OK) return st;
         ctx->stats.chunks++;
         maybe_flush(ctx);

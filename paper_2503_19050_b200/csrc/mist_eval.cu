@@ -824,7 +824,8 @@ k_eval(DevProblem P, EvalArgs A) {
         // the space (the dense mode still writes t, d, mem for it, with feasible = 0)
         const bool in_unit = kW <= (unsigned)P.kmax[0] && kA <= (unsigned)P.kmax[3];
         const bool twin = MODE != 1 && unit_ok && sT[tk].twin_T != ~0ull && sT[tk].twin_T >= A.twin_floor;
-        const bool active = unit_ok && (MODE == 1 || in_unit) && !twin;
+        const bool in_pass = MODE != 0 || !A.unit_pass || ((A.unit_pass == 1) == (!(kW & 1u) && !(kA & 1u)));
+        const bool active = unit_ok && (MODE == 1 || in_unit) && !twin && in_pass;
         const double dkW = kW, dkA = kA;
         const TupleConst& tc = sT[tk];
         const unsigned grp = tc.group;
@@ -1040,6 +1041,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
             bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
                           kAj <= (unsigned)P.kmax[3];                    // preset ranges
             if (active && sT[tkj].twin_T >= A.twin_floor && sT[tkj].twin_T != ~0ull) active = false;   // L20 twin
+            if (A.unit_pass && ((A.unit_pass == 1) != (!(kWj & 1u) && !(kAj & 1u)))) active = false;
             if (active && r7 && !P.ykey && !(A.no_r7 & 2) && tuple_cut(sT[tkj], fv.t, fv.y, fv.off[sT[tkj].group],
                                                      fv.off[sT[tkj].group + 1])) {
                 active = false;
@@ -1113,6 +1115,9 @@ k_eval_q(DevProblem P, EvalArgs A) {
             if (j == 0) { tk = tkj; kW = kWj; kA = kAj; g0 = g0j; excl = exj; }
         }
         if (CQ) __syncthreads();
+#ifdef MIST_DIAG_SETUP_ONLY
+        total = 0;                              // diagnostic build: window setup only, no runs
+#endif
         bool cv = false;                        // cached candidate (any group; emitted on group change)
         double ct = 0.0, cy = 0.0, cm = 0.0;
         u64 ci = 0;

@@ -133,6 +133,9 @@ struct EvalArgs {
     // L20 twins: a tuple with twin_T >= twin_floor is skipped (its twin is swept in
     // the same call); ~0 disables (fingerprints, MIST_DEDUP=0)
     unsigned long long twin_floor;
+    // unit passes of the frontier sweep: 0 = every unit; 1 = units with kW and kA both
+    // even; 2 = the others (their staircase then includes pass 1's frontier)
+    int unit_pass;
 };
 
 struct ReduceStats {
