@@ -562,8 +562,8 @@ static mist_status_t read_count(mist_ctx_t* ctx, SweepCtx& S, long long* out) {
 static mist_status_t write_count(mist_ctx_t* ctx, SweepCtx& S, long long v) {
     S.count = v;
     const u64 c = (u64)v;
+    // a pageable source is staged before cudaMemcpyAsync returns, so no sync is needed
     CK(cudaMemcpyAsync(S.d_count, &c, sizeof(u64), cudaMemcpyHostToDevice, ctx->stream), "set count");
-    CK(cudaStreamSynchronize(ctx->stream), "sync set count");
     return MIST_OK;
 }
 

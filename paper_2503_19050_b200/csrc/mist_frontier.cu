@@ -108,11 +108,42 @@ __global__ void k_scan_down(const u32* __restrict__ in, long long n, const u32* 
     }
 }
 
+// Small arrays (the per-group and per-chunk tables of a reduction): one CTA walks
+// the array in tiles of kScanTile with a running carry -- one launch instead of three.
+__global__ void k_scan_small(const u32* __restrict__ in, long long n, u32* __restrict__ out,
+                             u32* __restrict__ grand) {
+    __shared__ u32 wt[32];
+    u32 carry = 0;
+    for (long long base = 0; base < n; base += kScanTile) {
+        const long long b0 = base + (long long)threadIdx.x * kScanItems;
+        u32 v[kScanItems];
+        u32 s = 0;
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            v[j] = b0 + j < n ? in[b0 + j] : 0u;
+            s += v[j];
+        }
+        u32 total;
+        u32 run = block_excl_sum(s, wt, total) + carry;
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            if (b0 + j < n) out[b0 + j] = run;
+            run += v[j];
+        }
+        carry += total;
+    }
+    if (threadIdx.x == 0 && grand) *grand = carry;
+}
+
 // NOTE k_scan_reduce sums a tile in striped order and k_scan_down in blocked
 // order; both cover exactly the same index range [tile*kScanTile, +kScanTile).
 cudaError_t scan_u32_exclusive(cudaStream_t st, const u32* in, u32* out, long long n, u32* tmp,
                                u32* grand_total) {
     if (n <= 0) return cudaSuccess;
+    if (n <= 16 * kScanTile) {
+        k_scan_small<<<1, kThreads, 0, st>>>(in, n, out, grand_total);
+        return cudaGetLastError();
+    }
     const long long ntiles = (n + kScanTile - 1) / kScanTile;
     k_scan_reduce<<<(unsigned)ntiles, kThreads, 0, st>>>(in, n, tmp);
     k_scan_tiles<<<1, kThreads, 0, st>>>(tmp, ntiles, grand_total);
