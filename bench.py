@@ -41,18 +41,22 @@ WORKLOAD_TEXT = {
 }
 # SURVEY.md 8(d) per-unit figures: one Alg. 1 phase row costs ~56 FP64 lane-ops
 # branch-free with general factors (~4 channel + ~4 pattern + 3 rounds x 16 + 4
-# final) and ~7 with unit factors (channels + 3 max); the exact O9 memory of a
-# config ~10 (3 FMA, max, compare, per-run share).  The kernel counts the phase
-# rows it evaluates (stats phases_evaluated), so skipped work is not credited.
-def alg_ops(phases: int, configs: int, unit: bool) -> float:
-    return (7.0 if unit else 56.0) * phases + 10.0 * configs
+# final) and ~7 with unit factors (channels + 3 max).  An R5 lower-bound row
+# (DESIGN R5/R7: max of 4, pattern, 4 scaled channels, the first round's min, 4
+# DADD + 4 DFMA, max of 4) costs 25, the max alone 7 with unit factors.  The
+# kernel counts the rows it evaluates (stats phases_evaluated, bound_rows), so
+# skipped work is not credited.  (Round 1 also credited 10 lane-ops of O9 memory
+# per configuration; since R7/R9 most configurations are never touched, so that
+# term is gone -- the exact memory is a few FMAs per run.)
+def alg_ops(phases: int, bound_rows: int, unit: bool) -> float:
+    return (7.0 if unit else 56.0) * phases + (7.0 if unit else 25.0) * bound_rows
 
 
 # Static reference capture of the dominant kernel (one `ncu --set full` run of the
 # same workload, committed under profiles/): DRAM traffic and pipe figures cannot
 # be measured live without a profiler, so they are READ from that file at run time
 # and labelled as a reference capture, never as this run's measurement.
-NCU_CAPTURE = {2: "profiles/r2/ncu_k_eval_q_r2i_raw.csv"}
+NCU_CAPTURE = {2: "profiles/r2/ncu_k_eval_q_r2t_raw.csv"}
 _SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
           "ms": 1.0, "msecond": 1.0, "s": 1e3, "nsecond": 1e-6, "%": 1.0, "": 1.0}
 
@@ -292,7 +296,7 @@ def main():
     if rank == 0:
         # roofline of the dominant kernel (k_eval): algorithmic FP64 ops / eval time (this rank)
         my_configs = stats["configs_evaluated"]
-        ops = alg_ops(int(stats["phases_evaluated"]), my_configs, bool(stats["unit_factors"]))
+        ops = alg_ops(int(stats["phases_evaluated"]), int(stats["bound_rows"]), bool(stats["unit_factors"]))
         achieved = ops / (stats["eval_ms"] / 1e3) / 1e12
         peak = FP64_PEAK_OPS / 1e12
         ncu = ncu_reference(args.workload)
@@ -323,11 +327,13 @@ def main():
                          # tuples in, candidates out) from the committed capture, see "ncu"
                          "traffic": ncu["traffic"] if ncu else None,
                          "ncu": ncu,
-                         "kernel": "k_eval", "note": "FP64 lane-ops (FMA=1): SURVEY 8(d) per-unit figures (56 per "
-                         "Alg. 1 phase row, 7 with unit factors; 10 per config for O9 memory) x the phase rows "
-                         "the kernel counted + configs, / CUDA-event time of k_eval on the ctx stream; peak = "
-                         "148 SM x 64 FP64 lanes x 1.965 GHz (derived, DESIGN.md 4)",
+                         "kernel": "k_eval_q", "note": "FP64 lane-ops (FMA=1): SURVEY 8(d) per-unit figures (56 "
+                         "per Alg. 1 phase row, 25 per R5 bound row; 7 each with unit factors) x the rows the "
+                         "kernel counted, / CUDA-event time of the frontier eval kernel on the ctx stream; peak "
+                         "= 148 SM x 64 FP64 lanes x 1.965 GHz (derived, DESIGN.md 4). The exact skips (R2-R9) "
+                         "leave most configurations untouched, so this counts executed work only",
                          "phases_per_config": int(stats["phases_evaluated"]) / max(1, my_configs),
+                         "bound_rows_per_config": int(stats["bound_rows"]) / max(1, my_configs),
                          "eval_ms_per_step": stats["eval_ms"], "share_of_step": stats["eval_ms"] / max(1e-9, total_ms_last)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(stats["h2d_bytes"]),

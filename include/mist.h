@@ -151,6 +151,7 @@ typedef struct {
     uint64_t pilot_configs;      /* configs evaluated by the pilot (extra work, not in configs_evaluated) */
     int64_t rollbacks;           /* optimistic chunks re-run after a candidate-buffer overflow */
     uint64_t phases_evaluated;   /* Alg. 1 phase rows (PredINTF calls) the main eval kernel ran */
+    uint64_t bound_rows;         /* R5 lower-bound rows (DESIGN R5/R7) the main eval kernel ran */
 } mist_stats_t;
 /* total_ms spans the device work of the call from the moment its inputs are
  * resident in HBM to the last kernel (results still on the device). */

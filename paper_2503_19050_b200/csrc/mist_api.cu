@@ -697,7 +697,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     CK(ensure(ctx->foff, sizeof(int64_t) * ((size_t)pp.ng + 1)), "alloc filter offsets");
     S.d_count = (u64*)ctx->counters.p;
     S.d_phases = S.d_count + 1;
-    CK(cudaMemsetAsync(S.d_phases, 0, 6 * sizeof(u64), ctx->stream), "zero phase counters");
+    CK(cudaMemsetAsync(S.d_phases, 0, 7 * sizeof(u64), ctx->stream), "zero phase counters");
     S.d_foff = (int64_t*)ctx->foff.p;
     st = write_count(ctx, S, 0);
     if (st != MIST_OK) return st;
@@ -829,10 +829,11 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
     }
     ctx->stats.candidates += (uint64_t)S.count;   // before the final reduction
     {
-        u64 ph[6] = {0, 0, 0, 0, 0, 0};
+        u64 ph[7] = {0, 0, 0, 0, 0, 0, 0};
         CK(cudaMemcpyAsync(ph, S.d_phases, sizeof(ph), cudaMemcpyDeviceToHost, ctx->stream), "read phases");
         CK(cudaStreamSynchronize(ctx->stream), "sync phases");
         ctx->stats.phases_evaluated += ph[0];
+        ctx->stats.bound_rows += ph[6];
 #ifdef MIST_COUNTERS
         fprintf(stderr, "MIST_COUNTERS runs_backward=%llu runs_cut_at_k0=%llu d_evals=%llu k0_steps=%llu "
                 "runs_cut_r7=%llu configs=%llu\n",

@@ -552,7 +552,7 @@ __device__ __forceinline__ bool tuple_cut(const TupleConst& tc, const double* ft
 template <bool UNIT, bool NI = false>
 __device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst& tc, const UnitState& us, unsigned kW, unsigned kA,
                             unsigned g0, unsigned gend, const FGRow* FG, const double* ft, const double* fy,
-                            long long lo, long long hi, const unsigned* vals = nullptr) {
+                            long long lo, long long hi, unsigned& nlb, const unsigned* vals = nullptr) {
     // vals (pilot sub-grid): runs are indices into vals[] (ascending kG values)
     if (lo >= hi) return gend;
     const double dkA = kA;
@@ -565,8 +565,12 @@ __device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst&
     } else if (!(fy[hi - 1] <= 0.0)) {
         return gend;                           // no y = 0 point: nothing below every d
     }
+    const unsigned nrows = (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
+                           (unsigned)(tc.last != 0);
     auto cut = [&](unsigned g) -> bool {
-        const double lb = run_t_lb<UNIT, NI>(tc, us, (double)(vals ? vals[g] : g), dkA, FG) * (1.0 - 1e-12);
+        const unsigned kG = vals ? vals[g] : g;
+        if (kG != 0u) nlb += nrows;            // R5 rows (kG = 0 takes the R4 max)
+        const double lb = run_t_lb<UNIT, NI>(tc, us, (double)kG, dkA, FG) * (1.0 - 1e-12);
         if (!P.ykey) return ft[hi - 1] < lb;
         long long a = lo, b = hi;              // points with t < lb: [lo, a)
         while (a < b) {
@@ -677,7 +681,8 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
                                                 const UnitState& us, unsigned kW, unsigned kG, unsigned kA,
                                                 unsigned radix, double Q, int Q1, unsigned grp, const FGRow* FG,
                                                 bool cv, double ct, double cy, unsigned nrows, unsigned brows,
-                                                unsigned& nph, u64& fcnt, u64& fhash, const FiltView& fv,
+                                                unsigned& nph, unsigned& nlb, u64& fcnt, u64& fhash,
+                                                const FiltView& fv,
                                                 unsigned* ctr) {
     // the staircase filter runs in the frontier sweep and in the pilot (both exact, O10)
     constexpr bool FILT = MODE == 0 || MODE == 2;
@@ -749,6 +754,7 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             if (FILT && !P.ykey) {
                 double scale;
                 const double lb = d_lower_bound<UNIT, NI>(tc, us, rs, kO, FG, scale);
+                nlb += nrows;
                 const double thr = best_y < y_thr ? best_y : y_thr;
                 if (lb - 1e-12 * scale > thr) {
                     if (A.fp) continue;                       // keep counting feasible configs
@@ -825,7 +831,10 @@ k_eval(DevProblem P, EvalArgs A) {
         const bool in_unit = kW <= (unsigned)P.kmax[0] && kA <= (unsigned)P.kmax[3];
         const bool twin = MODE != 1 && unit_ok && sT[tk].twin_T != ~0ull && sT[tk].twin_T >= A.twin_floor;
         const bool in_pass = MODE != 0 || !A.unit_pass || ((A.unit_pass == 1) == (!(kW & 1u) && !(kA & 1u)));
-        const bool active = unit_ok && (MODE == 1 || in_unit) && !twin && in_pass;
+        // tuple-level R7 (ykey = d) in the frontier and pilot modes
+        const bool tcut = MODE != 1 && unit_ok && !P.ykey && A.f_off && !A.fp && !(A.no_r7 & 3) &&
+                          tuple_cut(sT[tk], A.f_t, A.f_y, A.f_off[sT[tk].group], A.f_off[sT[tk].group + 1]);
+        const bool active = unit_ok && (MODE == 1 || in_unit) && !twin && in_pass && !tcut;
         const double dkW = kW, dkA = kA;
         const TupleConst& tc = sT[tk];
         const unsigned grp = tc.group;
@@ -833,9 +842,10 @@ k_eval(DevProblem P, EvalArgs A) {
         if (active) unit_forward<UNIT>(tc, dkW, dkA, FG, us);
         // R7 (frontier and pilot modes): runs ig >= icut are beaten by the staircase on t alone
         unsigned icut = radix;
+        unsigned nlb = 0;                      // R5 bound rows evaluated (roofline count)
         if (MODE != 1 && active && A.f_off && !A.fp && !(A.no_r7 & 1))
             icut = run_cut<UNIT>(P, tc, us, kW, kA, 0u, radix, FG, A.f_t, A.f_y, A.f_off[grp], A.f_off[grp + 1],
-                                 MODE == 2 ? A.vals : nullptr);
+                                 nlb, MODE == 2 ? A.vals : nullptr);
         // phase rows evaluated by this thread (PredINTF calls), for the roofline's algorithmic count
         const unsigned nrows = (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
                                (unsigned)(tc.last != 0);
@@ -878,7 +888,7 @@ k_eval(DevProblem P, EvalArgs A) {
                     FiltView fv;
                     fv.t = A.f_t; fv.y = A.f_y; fv.idx = A.f_idx; fv.off = A.f_off;
                     const RunCand rc = frontier_run<UNIT, MODE>(P, A, tc, us, kW, kG, kA, radix, Q, Q1, grp, FG, cv,
-                                                                ct, cy, nrows, brows, nph, fcnt, fhash, fv, ctr);
+                                                                ct, cy, nrows, brows, nph, nlb, fcnt, fhash, fv, ctr);
                     has = rc.has; best_y = rc.y; best_i = rc.idx; best_m = rc.m; rs.t = rc.t;
                 }
                 if (MODE != 1 && has) {
@@ -899,11 +909,15 @@ k_eval(DevProblem P, EvalArgs A) {
         }
         if (MODE != 1) {
             warp_emit(cv, ct, cy, cm, ci, grp, A, lane);
-            if (A.phases) {                                   // warp-reduced phase-row count
-                unsigned v = nph;
+            if (A.phases) {                                   // warp-reduced phase-row counts
+                unsigned v = nph, b = nlb;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                for (int o = 16; o > 0; o >>= 1) {
+                    v += __shfl_xor_sync(0xffffffffu, v, o);
+                    b += __shfl_xor_sync(0xffffffffu, b, o);
+                }
                 if (lane == 0 && v) atomicAdd(A.phases, (u64)v);
+                if (lane == 0 && b) atomicAdd(A.phases + 6, (u64)b);
             }
             flush_ctr(A, ctr, lane);
             if (A.fp) {
@@ -973,7 +987,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
     const unsigned radix = (unsigned)Q1;
     const unsigned upt = A.upt;
     const u64 n_units = A.n_units;
-    unsigned nph = 0;
+    unsigned nph = 0, nlb = 0;
     unsigned ctr[5] = {0u, 0u, 0u, 0u, 0u};
     // CQ: the window's tuples arrive by one TMA bulk copy, issued one window ahead
     auto tuples_of = [&](u64 b, u64& t0, int& nt) {
@@ -1076,7 +1090,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                     // fingerprints, which count every feasible config)
                     if (r7 && g0j < gend) {
                         g1j = run_cut<UNIT, NI>(P, tc, us, kWj, kAj, g0j, gend, FG, fv.t, fv.y, fv.off[tc.group],
-                                            fv.off[tc.group + 1]);
+                                                fv.off[tc.group + 1], nlb);
                         MIST_CTR(4, gend - g1j);
                     }
                 }
@@ -1171,7 +1185,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                 const bool same = cv && cgrp == grp;
                 u64 fcnt = 0, fhash = 0;
                 const RunCand rc = frontier_run<UNIT, 0, NI>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
-                                                         ct, cy, nrows, brows, nph, fcnt, fhash, fv, ctr);
+                                                         ct, cy, nrows, brows, nph, nlb, fcnt, fhash, fv, ctr);
                 if (A.fp && fcnt) {
                     atomicAdd(A.fp + 2 * (u64)grp, fcnt);
                     atomicAdd(A.fp + 2 * (u64)grp + 1, fhash);
@@ -1195,10 +1209,14 @@ k_eval_q(DevProblem P, EvalArgs A) {
         warp_emit(cv, ct, cy, cm, ci, cgrp, A, lane);
     }
     if (A.phases) {
-        unsigned v = nph;
+        unsigned v = nph, b = nlb;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
         if (lane == 0 && v) atomicAdd(A.phases, (u64)v);
+        if (lane == 0 && b) atomicAdd(A.phases + 6, (u64)b);
     }    flush_ctr(A, ctr, lane);
 }
 

@@ -88,7 +88,7 @@ class mist_stats_t(C.Structure):
                 ("reductions", C.c_int64), ("sort_keys", C.c_uint64), ("sort_passes", C.c_int32),
                 ("unit_factors", C.c_int32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("pilot_ms", C.c_double), ("pilot_configs", C.c_uint64), ("rollbacks", C.c_int64),
-                ("phases_evaluated", C.c_uint64)]
+                ("phases_evaluated", C.c_uint64), ("bound_rows", C.c_uint64)]
 
 
 MAX_STAGES = 128
