@@ -71,14 +71,14 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defs=No
                    "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc,
                    "-c", src, "-o", obj]
         else:
-            cmd = ["g++", *defs, "-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", CSRC,
+            cmd = ["g++", *defs, "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-I", INCLUDE, "-I", CSRC,
                    "-I", "/usr/local/cuda/include", "-I", nccl_inc, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = lib_path + ".tmp"
-    cmd = ["nvcc", *ARCH, "-shared", "-o", tmp, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
+    cmd = ["nvcc", *ARCH, "-shared", "-o", tmp, *objs, "-L", nccl_lib, "-l:libnccl.so.2", "-lgomp",
            "-Xlinker", "-rpath," + nccl_lib, "-cudart", "static"]
     if verbose:
         print(" ".join(cmd), flush=True)

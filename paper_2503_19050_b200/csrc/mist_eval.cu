@@ -1045,13 +1045,25 @@ k_eval_q(DevProblem P, EvalArgs A) {
         unsigned total = 0;
         // per-thread state of unit j = 0 (the warp queue of the non-CQ path reads it)
         unsigned tk = 0, kW = 0, kA = 0, g0 = radix, excl = 0;
+        // 32-bit unit decode: base sits r0 units into tuple tb0, so unit w of the window is
+        // unit (r0 + w) mod upt of tuple tb0 + (r0 + w) / upt; both divisions by a float
+        // reciprocal with a one-step correction (exact for these small operands)
+        const unsigned r0 = (unsigned)(base - tb0 * (u64)upt);
+        const float inv_upt = 1.0f / (float)upt, inv_rad = 1.0f / (float)radix;
 #pragma unroll
         for (int j = 0; j < UPW; ++j) {
             const unsigned w = (unsigned)(j * NT + tid);                   // unit of the window
             const u64 u = base + w;
-            const unsigned tkj = u < n_units ? (unsigned)(u / upt - tb0) : 0u;
-            const unsigned jj = (unsigned)(u - (tb0 + tkj) * (u64)upt);
-            const unsigned kWj = jj / radix, kAj = jj - kWj * radix;
+            const unsigned off = r0 + w;
+            unsigned tq = (unsigned)((float)off * inv_upt);
+            tq -= tq * upt > off ? 1u : 0u;
+            tq += (tq + 1u) * upt <= off ? 1u : 0u;
+            const unsigned tkj = u < n_units ? tq : 0u;
+            const unsigned jj = off - tq * upt;
+            unsigned kWj = (unsigned)((float)jj * inv_rad);
+            kWj -= kWj * radix > jj ? 1u : 0u;
+            kWj += (kWj + 1u) * radix <= jj ? 1u : 0u;
+            const unsigned kAj = jj - kWj * radix;
             bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
                           kAj <= (unsigned)P.kmax[3];                    // preset ranges
             if (active && sT[tkj].twin_T >= A.twin_floor && sT[tkj].twin_T != ~0ull) active = false;   // L20 twin

@@ -23,6 +23,7 @@
 // "first" stage at step k gives S = k.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <atomic>
 #include <cmath>
 #include <limits>
@@ -202,6 +203,137 @@ Result solve_G(const Problem& pb, int G, double inc) {
     return best;
 }
 
+// The same DP with the work of each step spread over threads (OpenMP), results
+// independent of the thread count.  Per step: (1) node ids of the current labels,
+// in state order; (2) closing stages, per source state in parallel, reduced in
+// state order with strict < (the plan the sequential loop finds first among
+// equal values); (3) extensions grouped by destination state, each destination
+// built by one thread from its sources in state order and filtered.  The
+// incumbent of (3) is the one after all of step k's closes, tighter than or equal
+// to the sequential loop's: pruning stays exact.
+Result solve_G_par(const Problem& pb, int G, double inc, int nthreads) {
+    Result best;
+    best.val = inc;
+    const double G1 = (double)(G - 1);
+    const int L = pb.L, D = pb.devices;
+    const int Smax = std::min(L, D);
+    std::vector<Node> nodes;
+    std::map<std::pair<int, int>, State> cur, nxt;
+    cur[{0, 0}].v.push_back(Label{0.0, 0.0, 0.0, -1, -1, -1});
+    int32_t close_parent = -1, close_g = -1, close_p = -1, close_k = 0;
+    struct Src { int lu, du; std::vector<Label>* labs; std::vector<int32_t> nid; };
+    struct Task { int si; int32_t g; };
+    struct Close { double val; int32_t parent, g, p; };
+    for (int k = 1; k <= Smax && !cur.empty(); ++k) {
+        const int w = std::min(G, k), last = k == 1;
+        std::vector<Src> src;
+        src.reserve(cur.size());
+        for (auto& st : cur) {
+            Src sc{st.first.first, st.first.second, &st.second.v, {}};
+            sc.nid.resize(sc.labs->size());
+            for (size_t i = 0; i < sc.labs->size(); ++i) {
+                const Label& lb = (*sc.labs)[i];
+                if (lb.g < 0) { sc.nid[i] = -1; continue; }
+                sc.nid[i] = (int32_t)nodes.size();
+                nodes.push_back(Node{lb.parent, lb.g, lb.p});
+            }
+            src.push_back(std::move(sc));
+        }
+        // (2) close the plan: this stage is stage 1 (first) and S = k
+        std::vector<Close> closes(src.size(), Close{std::numeric_limits<double>::infinity(), -1, -1, -1});
+        const double inc_k = best.val;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+        for (long long si = 0; si < (long long)src.size(); ++si) {
+            const Src& sc = src[(size_t)si];
+            Close c{inc_k, -1, -1, -1};
+            const int lrem = L - sc.lu, drem = D - sc.du;
+            for (auto& nm : pb.meshes) {
+                if (nm.first * nm.second != drem) continue;
+                const int32_t g = pb.find(G, 1, last, w, lrem, nm.first, nm.second);
+                if (g < 0) continue;
+                const int64_t a = pb.offs[g], b = pb.offs[g + 1];
+                for (size_t i = 0; i < sc.labs->size(); ++i) {
+                    const Label& lb = (*sc.labs)[i];
+                    for (int64_t q = a; q < b; ++q) {
+                        const double t = pb.pts[q].t, d = pb.pts[q].y;
+                        const double S2 = lb.S + t, M2 = std::max(lb.M, d + S2), T2 = std::max(lb.T, t);
+                        const double val = G1 * T2 + M2;
+                        if (val < c.val) c = Close{val, sc.nid[i], g, (int32_t)(q - a)};
+                    }
+                }
+            }
+            closes[(size_t)si] = c;
+        }
+        for (size_t si = 0; si < src.size(); ++si)
+            if (closes[si].g >= 0 && closes[si].val < best.val) {
+                best.val = closes[si].val;
+                close_parent = closes[si].parent; close_g = closes[si].g; close_p = closes[si].p; close_k = k;
+            }
+        nxt.clear();
+        if (k < Smax) {
+            // (3) extensions, grouped by destination state
+            std::map<std::pair<int, int>, std::vector<Task>> dest;
+            for (size_t si = 0; si < src.size(); ++si) {
+                const int lrem = L - src[si].lu, drem = D - src[si].du;
+                for (int l = 1; l <= lrem - 1; ++l)
+                    for (auto& nm : pb.meshes) {
+                        const int sz = nm.first * nm.second;
+                        if (sz > drem - 1) continue;
+                        const int32_t g = pb.find(G, 0, last, w, l, nm.first, nm.second);
+                        if (g < 0) continue;
+                        dest[{src[si].lu + l, src[si].du + sz}].push_back(Task{(int)si, g});
+                    }
+            }
+            std::vector<std::pair<std::pair<int, int>, std::vector<Task>*>> dl;
+            dl.reserve(dest.size());
+            for (auto& e : dest) dl.push_back({e.first, &e.second});
+            std::vector<std::vector<Label>> out(dl.size());
+            const double inc_x = best.val;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+            for (long long di = 0; di < (long long)dl.size(); ++di) {
+                std::vector<Label>& o = out[(size_t)di];
+                size_t thr = 4096;
+                for (const Task& tk : *dl[(size_t)di].second) {
+                    const Src& sc = src[(size_t)tk.si];
+                    const int64_t a = pb.offs[tk.g], b = pb.offs[tk.g + 1];
+                    for (size_t i = 0; i < sc.labs->size(); ++i) {
+                        const Label& lb = (*sc.labs)[i];
+                        if (G1 * lb.T + lb.M >= inc_x) continue;
+                        for (int64_t q = a; q < b; ++q) {
+                            const double t = pb.pts[q].t, d = pb.pts[q].y;
+                            const double S2 = lb.S + t, M2 = std::max(lb.M, d + S2), T2 = std::max(lb.T, t);
+                            if (G1 * T2 + M2 >= inc_x) continue;
+                            o.push_back(Label{S2, M2, T2, sc.nid[i], tk.g, (int32_t)(q - a)});
+                        }
+                    }
+                    if (o.size() > thr) {
+                        pareto_filter(o, G1, inc_x);
+                        thr = 2 * o.size() + 4096;
+                    }
+                }
+                pareto_filter(o, G1, inc_x);
+            }
+            for (size_t di = 0; di < dl.size(); ++di) {
+                if (out[di].empty()) continue;
+                best.labels += (int64_t)out[di].size();
+                nxt[dl[di].first].v = std::move(out[di]);
+            }
+        }
+        std::swap(cur, nxt);
+    }
+    if (close_k > 0) {
+        best.G = G;
+        best.S = close_k;
+        best.g.push_back(close_g);
+        best.p.push_back(close_p);
+        for (int32_t nd = close_parent; nd >= 0; nd = nodes[nd].parent) {
+            best.g.push_back(nodes[nd].g);
+            best.p.push_back(nodes[nd].p);
+        }
+    }
+    return best;
+}
+
 }  // namespace
 
 extern "C" mist_status_t mist_solve_inter(const mist_group_t* groups, int64_t n_groups, const mist_point_t* points,
@@ -293,7 +425,21 @@ extern "C" mist_status_t mist_solve_inter(const mist_group_t* groups, int64_t n_
     const double inc = std::nextafter(seed, std::numeric_limits<double>::infinity());
 
     std::vector<Result> res;
-    run_all(pb, inc, res);
+    const char* par_env = getenv("MIST_INTER_PAR");
+    if (par_env && !strcmp(par_env, "G")) {
+        run_all(pb, inc, res);   // round-1 scheme: one G per thread, the single-stage seed as incumbent
+    } else {
+        // G by G in ascending order, each DP spread over every thread, with the best plan so
+        // far as the incumbent: a G whose plans cannot beat it prunes everything early.
+        // Strict improvement only, so ties keep the smaller G (processed first).
+        const unsigned nthr = n_threads > 0 ? (unsigned)n_threads : std::max(1u, std::thread::hardware_concurrency());
+        res.assign(Gs.size(), Result());
+        double incumbent = inc;
+        for (size_t i = 0; i < Gs.size(); ++i) {
+            res[i] = solve_G_par(pb, Gs[i], incumbent, (int)nthr);
+            if (res[i].S > 0) incumbent = std::min(incumbent, res[i].val);
+        }
+    }
 
     int best = -1;
     int64_t labels = 0;

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--fingerprints", action="store_true")
     ap.add_argument("--plan", action="store_true", help="rank 0 also solves the inter-stage plan (Eq. 2-3)")
+    ap.add_argument("--plan-ab", action="store_true", help="with --plan: both solver schemes on the same frontier")
     ap.add_argument("--warmup", type=int, default=1,
                     help="untimed sweeps of a small tuple range first (NCCL connection setup, allocations)")
     args = ap.parse_args()
@@ -74,13 +75,17 @@ def main():
         print(json.dumps(out), flush=True)
         if args.plan:
             pb = workload(args.workload, factors=args.factors)
-            ts = time.perf_counter()
-            plan = mist.mist_solve_inter(spec.groups, pts, offs, pb.model.L, pb.N * pb.M)
-            el = time.perf_counter() - ts
-            print(json.dumps({"plan": {"solve_s": el, "G": plan["G"], "S": plan["S"],
-                                       "objective_s": plan["objective"], "labels": int(plan["labels"]),
-                                       "sweep_to_plan_s": float(w[0]) + el,
-                                       "host_threads": os.cpu_count()}}), flush=True)
+            # --plan-ab: also the round-1 scheme (one G per thread), same frontier, for A/B
+            modes = ["", "G"] if args.plan_ab else [os.environ.get("MIST_INTER_PAR", "")]
+            for mode in modes:
+                os.environ["MIST_INTER_PAR"] = mode
+                ts = time.perf_counter()
+                plan = mist.mist_solve_inter(spec.groups, pts, offs, pb.model.L, pb.N * pb.M)
+                el = time.perf_counter() - ts
+                print(json.dumps({"plan": {"solve_s": el, "G": plan["G"], "S": plan["S"],
+                                           "objective_s": plan["objective"], "labels": int(plan["labels"]),
+                                           "sweep_to_plan_s": float(w[0]) + el, "scheme": mode or "G-serial",
+                                           "host_threads": os.cpu_count()}}), flush=True)
         if args.out:
             np.savez_compressed(args.out, points=pts, offsets=offs, fp_count=fc, fp_hash=fh)
     ctx.close()
