@@ -253,6 +253,8 @@ struct UnitState {
 // Per-run state: everything that does not depend on kO.
 struct RunState {
     double t, dbase;
+    double dsc;                     // deferred B' (DEFER): rounding scale of the lower-bound dbase
+    bool dexact;                    // dbase is exact (else a lower bound from R5 rows of B')
     double FpH_L, FpD_L0, FpD_L1;   // F' layer H2D / D2H at kO = 0
     double FpH_E, FpD_E, FpH_H, FpD_H;
     double Kf, Kb;                  // D*Mem_fwd / D*Mem_bwd without the (Q-kO), kO terms
@@ -370,36 +372,76 @@ __device__ __noinline__ double block_backward(const BlockConst& b, bool r1, doub
     return TB;
 }
 
-// Stable phases of the run: t (Eq. 5) and the kO-independent part of d (Eq. 6).
+// Deferred B' (DEFER): B's exact row and, when B' differs (z < 2 at DP > 1), only
+// the R5 bound of B' -- d's backward part T(B') - T(B) >= lb(B') - T(B).  The bound
+// test of the first configs runs on that lower bound; a run that survives it gets
+// the exact B' rows (run_dbase_exact) before any d is evaluated, so every cut is
+// exact and every d is the same as without deferral.
+template <bool UNIT, bool NI>
+__device__ __forceinline__ double lb_row(double x0, double x1, double x2, double x3, const FGRow* FG);
+
 template <bool UNIT>
+__device__ __noinline__ double block_backward_lb(const BlockConst& b, bool r1, double FH, double kG, double kA,
+                                                 const FGRow* FG, double& dBp_lb) {
+    const double sAh = r1 ? b.sAh1 : b.sAh;
+    const double CB = r1 ? b.C_B1 : b.C_B;
+    const double BH = FH + kG * b.sGh + kA * sAh, BD = kG * b.sGd;
+    const double TB = pred_intf<UNIT>(CB, b.N_B, BH, BD, FG);
+    dBp_lb = (b.N_Bp == b.N_B) ? 0.0 : lb_row<UNIT, false>(CB, b.N_Bp, BH, BD, FG) - TB;
+    return TB;
+}
+
+// exact sum count (T(B') - T(B)), the same operations in the same order as run_backward
+template <bool UNIT>
+__device__ __noinline__ double run_dbase_exact(const TupleConst& tc, const UnitState& us, double kG, double kA,
+                                               const FGRow* FG) {
+    double db = 0.0, dBp;
+    if (tc.nl0 > 0.0) { block_backward<UNIT>(tc.L, false, us.FH_L, kG, kA, FG, dBp); db += tc.nl0 * dBp; }
+    if (tc.nl1 > 0.0) { block_backward<UNIT>(tc.L, true, us.FH_L, kG, kA, FG, dBp); db += tc.nl1 * dBp; }
+    if (tc.first) { block_backward<UNIT>(tc.E, false, us.FH_E, kG, kA, FG, dBp); db += dBp; }
+    if (tc.last) { block_backward<UNIT>(tc.H, false, us.FH_H, kG, kA, FG, dBp); db += dBp; }
+    return db;
+}
+
+// Stable phases of the run: t (Eq. 5) and the kO-independent part of d (Eq. 6).
+template <bool UNIT, bool DEFER = false>
 __device__ __forceinline__ void run_backward(const TupleConst& tc, const UnitState& us, double kW, double kG,
                                              double kA, const FGRow* FG, RunState& rs) {
-    double tb = 0.0, db = 0.0, dBp;
+    double tb = 0.0, db = 0.0, dBp, dsc = 0.0;
+    bool exact = true;
+    auto bb = [&](const BlockConst& b, bool r1, double FH) -> double {
+        if (!DEFER) return block_backward<UNIT>(b, r1, FH, kG, kA, FG, dBp);
+        const double TB = block_backward_lb<UNIT>(b, r1, FH, kG, kA, FG, dBp);
+        if (b.N_Bp != b.N_B) { exact = false; dsc += fabs(dBp) + 2.0 * TB; }
+        return TB;
+    };
     rs.FpH_L = us.FH_L + kG * tc.L.sGh;
     rs.FpD_L0 = us.FD_L0 + kW * tc.L.sWd;
     rs.FpD_L1 = us.FD_L1 + kW * tc.L.sWd;
     if (tc.nl0 > 0.0) {
-        tb += tc.nl0 * block_backward<UNIT>(tc.L, false, us.FH_L, kG, kA, FG, dBp);
+        tb += tc.nl0 * bb(tc.L, false, us.FH_L);
         db += tc.nl0 * dBp;
     }
     if (tc.nl1 > 0.0) {
-        tb += tc.nl1 * block_backward<UNIT>(tc.L, true, us.FH_L, kG, kA, FG, dBp);
+        tb += tc.nl1 * bb(tc.L, true, us.FH_L);
         db += tc.nl1 * dBp;
     }
     if (tc.first) {
-        tb += block_backward<UNIT>(tc.E, false, us.FH_E, kG, kA, FG, dBp);
+        tb += bb(tc.E, false, us.FH_E);
         db += dBp;
         rs.FpH_E = us.FH_E + kG * tc.E.sGh;
         rs.FpD_E = us.FD_E + kW * tc.E.sWd;
     }
     if (tc.last) {
-        tb += block_backward<UNIT>(tc.H, false, us.FH_H, kG, kA, FG, dBp);
+        tb += bb(tc.H, false, us.FH_H);
         db += dBp;
         rs.FpH_H = us.FH_H + kG * tc.H.sGh;
         rs.FpD_H = us.FD_H + kW * tc.H.sWd;
     }
     rs.t = (unit_tf(tc, us) + tb) + tc.t_p2p;
     rs.dbase = db;                   // d = db + sum count * (T(F') - T(F)), block by block (Eq. 6)
+    rs.dexact = exact;
+    rs.dsc = dsc * (tc.nl0 + tc.nl1 + 2.0);   // counts multiply the per-block terms
 }
 
 // d of config kO of the run: first-microbatch forward F' of every block (Eq. 6).
@@ -703,8 +745,14 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
         // D*mem is non-increasing in kO (O9: P_raw >= min(l,2) P_layer), so the
         // feasible configs of a run are a suffix in kO and a run whose kO = Q
         // config is over budget has none: its t and d are never needed (R2).
+#ifdef MIST_DEFER_BP
+        run_backward<UNIT, true>(tc, us, dkW, dkG, dkA, FG, rs);
+        nph += nrows;
+        if (!rs.dexact) nlb += brows - nrows;
+#else
         run_backward<UNIT>(tc, us, dkW, dkG, dkA, FG, rs);
         nph += brows;
+#endif
         MIST_CTR(0, 1);
         // Bound-and-skip (ykey = d): a config whose lower bound of d exceeds the
         // best d the run already has, or the y of a known feasible point with
@@ -753,10 +801,21 @@ __device__ __forceinline__ RunCand frontier_run(const DevProblem& P, const EvalA
             const u64 idx = idx0 + (u64)ko * Q1;
             if (FILT && !P.ykey) {
                 double scale;
-                const double lb = d_lower_bound<UNIT, NI>(tc, us, rs, kO, FG, scale);
+                double lb = d_lower_bound<UNIT, NI>(tc, us, rs, kO, FG, scale);
                 nlb += nrows;
                 const double thr = best_y < y_thr ? best_y : y_thr;
-                if (lb - 1e-12 * scale > thr) {
+                bool over = lb - 1e-12 * (scale + rs.dsc) > thr;
+                if (!over && !rs.dexact) {
+                    // the lower-bound dbase did not cut: the exact B' rows, then the same test
+                    rs.dbase = run_dbase_exact<UNIT>(tc, us, dkG, dkA, FG);
+                    rs.dexact = true;
+                    rs.dsc = 0.0;
+                    nph += brows;
+                    lb = d_lower_bound<UNIT, NI>(tc, us, rs, kO, FG, scale);
+                    nlb += nrows;
+                    over = lb - 1e-12 * scale > thr;
+                }
+                if (over) {
                     if (A.fp) continue;                       // keep counting feasible configs
                     // the bound is non-decreasing in kO while the F' nonzero pattern is fixed,
                     // which holds for kO >= 1 (H2D and D2H grow with kO); at kO = 0 a zero
