@@ -216,3 +216,23 @@ def test_solver_many_points_per_group(monkeypatch, thin):
         arr, offs = _csr(pts)
         plan = mist.mist_solve_inter(mist.group_array(keys), arr, offs, 3, 2)
         _check_plan(plan, keys, pts, 3, 2, want)
+
+
+@pytest.mark.parametrize("scheme", ["", "G"])
+def test_solver_plan_independent_of_threads(monkeypatch, scheme):
+    """The plan (not only its value) is the same for every thread count: the
+    per-step parallel DP (default) reduces its closing stages in state order and
+    builds each destination state on one thread."""
+    monkeypatch.setenv("MIST_INTER_PAR", scheme)
+    pb = tiny(6, 4, 1, 2, 2, 2)
+    keys = _tiny_keys(pb)
+    L, devices = pb.model.L, pb.N * pb.M
+    for rep in range(4):
+        pts = random_candidates(keys, seed=900 + rep, max_points=6, p_empty=0.05)
+        arr, offs = _csr(pts)
+        groups = mist.group_array(keys)
+        plans = [mist.mist_solve_inter(groups, arr, offs, L, devices, n_threads=nt) for nt in (1, 2, 5)]
+        for p in plans[1:]:
+            assert (p["G"], p["S"], p["objective"]) == (plans[0]["G"], plans[0]["S"], plans[0]["objective"])
+            assert p["group"].tolist() == plans[0]["group"].tolist()
+            assert p["point"].tolist() == plans[0]["point"].tolist()
