@@ -33,9 +33,9 @@ void pack_problem(const mist_model_t*, int64_t, const mist_mesh_t*, const mist_s
 int coef_row(const mist_coeffs_t*, int, int);
 // from mist_eval.cu
 cudaError_t launch_precompute(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
-                              u64, u64, TupleConst*);
+                              u64, u64, TupleConst*, bool);
 cudaError_t launch_precompute_segs(cudaStream_t, int, const DevProblem&, const DevGroup*, int, const double*,
-                                   const u64*, int, u64, TupleConst*);
+                                   const u64*, int, u64, TupleConst*, bool);
 cudaError_t launch_eval(cudaStream_t, int, const DevProblem&, const EvalArgs&, int);
 cudaError_t launch_pilot_zero(cudaStream_t, int, const DevProblem&, const EvalArgs&);
 size_t eval_smem_bytes(unsigned upt);
@@ -428,7 +428,7 @@ static mist_status_t dense_eval(mist_ctx_t* ctx, const Prepared& pp, u64 begin, 
         const u64 nT = std::min<u64>(chunk_T, T_e - T0);
         int h = ev_begin(ctx, CAT_PRE);
         CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, T0, nT,
-                             (TupleConst*)ctx->tuples.p), "precompute");
+                             (TupleConst*)ctx->tuples.p, false), "precompute");
         ev_end(ctx, h);
         EvalArgs A;
         std::memset(&A, 0, sizeof(A));
@@ -730,6 +730,8 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
         }
     }
     for (auto& nv : levels) nv = std::min(nv, Q + 1);
+    const char* henv = getenv("MIST_HALVES");
+    const bool halves = henv && henv[0] == '1';
     const char* penv = getenv("MIST_PASSES");
     const int passes = (penv && penv[0] == '2') ? 2 : 1;
     const char* zenv = getenv("MIST_PILOT_ZERO");
@@ -742,7 +744,7 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
         if (ch.size() == 1) {
             const auto& seg = ch[0];
             CK(launch_precompute(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef, seg.first,
-                                 seg.second - seg.first, (TupleConst*)ctx->tuples.p), "precompute");
+                                 seg.second - seg.first, (TupleConst*)ctx->tuples.p, halves), "precompute");
             nT = seg.second - seg.first;
         } else {
             // a block-cyclic share: every segment in one launch (segment table uploaded once)
@@ -758,7 +760,8 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
             CK(cudaMemcpyAsync(ctx->segs.p, tab.data(), sizeof(u64) * tab.size(), cudaMemcpyHostToDevice,
                                ctx->stream), "upload segs");
             CK(launch_precompute_segs(ctx->stream, ctx->device, pp.P, pp.d_groups, pp.ng, pp.d_coef,
-                                      (const u64*)ctx->segs.p, (int)ch.size(), nT, (TupleConst*)ctx->tuples.p),
+                                      (const u64*)ctx->segs.p, (int)ch.size(), nT, (TupleConst*)ctx->tuples.p,
+                                      halves),
                "precompute");
         }
         ctx->stats.kernel_launches += 1;
@@ -811,7 +814,19 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
                 ctx->stats.pilot_configs += nT * (u64)nv * nv * nv * nv;
             }
         }
-        if (passes == 2) {
+        if (halves) {
+            // the even tuples of every group first (the first half of the table), then a
+            // reduction, so the odd half sweeps against a staircase that already holds
+            // real frontier points of its groups
+            const u64 h = (nT + 1) / 2;
+            st = eval_opt(ctx, S, 0, tup, 0, h, 0, nullptr);
+            if (st != MIST_OK) return st;
+            if (S.count > 0) {
+                st = reduce_buffer(ctx, S);
+                if (st != MIST_OK) return st;
+            }
+            st = eval_opt(ctx, S, 0, tup, h, nT, 0, nullptr);
+        } else if (passes == 2) {
             // pass 1 (units with kW, kA even) refines the staircase that pass 2 filters with
             st = eval_opt(ctx, S, 0, tup, 0, nT, 0, nullptr, 1);
             if (st != MIST_OK) return st;

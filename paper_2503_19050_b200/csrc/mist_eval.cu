@@ -148,10 +148,20 @@ __device__ void make_tuple(const DevProblem& P, const DevGroup* groups, int ng,
 // a2 over a rank's block-cyclic share: seg[2*s] = first tuple of segment s,
 // seg[2*s+1] = its first position in `out` (prefix of the segment lengths,
 // seg[2*nseg+1] = total); one launch for all segments.
+// Table position of the logical tuple j when `halves` is set: the even logical
+// positions fill the first half of the table, the odd ones the second, so a sweep of
+// the first half refines the staircase of every group before the second half runs.
+__device__ __forceinline__ u64 half_order(u64 i, u64 nT, bool halves) {
+    if (!halves) return i;
+    const u64 h = (nT + 1) / 2;
+    return i < h ? 2 * i : 2 * (i - h) + 1;
+}
+
 __global__ void k_tuple_precompute_segs(DevProblem P, const DevGroup* __restrict__ groups, int ng,
                                         const double* __restrict__ coef, const u64* __restrict__ seg, int nseg,
-                                        u64 nT, TupleConst* __restrict__ out) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nT; i += (u64)gridDim.x * blockDim.x) {
+                                        u64 nT, TupleConst* __restrict__ out, bool halves) {
+    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < nT; o += (u64)gridDim.x * blockDim.x) {
+        const u64 i = half_order(o, nT, halves);
         int lo = 0, hi = nseg - 1;                  // last segment whose first position <= i
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -159,17 +169,17 @@ __global__ void k_tuple_precompute_segs(DevProblem P, const DevGroup* __restrict
         }
         TupleConst tc;
         make_tuple(P, groups, ng, coef, seg[2 * lo] + (i - seg[2 * lo + 1]), tc);
-        out[i] = tc;
+        out[o] = tc;
     }
 }
 
 __global__ void k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ groups, int ng,
                                    const double* __restrict__ coef, u64 T0, u64 nT,
-                                   TupleConst* __restrict__ out) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nT; i += (u64)gridDim.x * blockDim.x) {
+                                   TupleConst* __restrict__ out, bool halves) {
+    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < nT; o += (u64)gridDim.x * blockDim.x) {
         TupleConst tc;
-        make_tuple(P, groups, ng, coef, T0 + i, tc);
-        out[i] = tc;
+        make_tuple(P, groups, ng, coef, T0 + half_order(o, nT, halves), tc);
+        out[o] = tc;
     }
 }
 
@@ -1410,24 +1420,25 @@ static int sm_count(int device) {
 }
 
 cudaError_t launch_precompute(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,
-                              int ng, const double* coef, u64 T0, u64 nT, TupleConst* out) {
+                              int ng, const double* coef, u64 T0, u64 nT, TupleConst* out, bool halves) {
     if (nT == 0) return cudaSuccess;
     const int threads = 128;
     u64 blocks = (nT + threads - 1) / threads;
     const u64 cap = (u64)sm_count(device) * 16;
     if (blocks > cap) blocks = cap;
-    k_tuple_precompute<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, T0, nT, out);
+    k_tuple_precompute<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, T0, nT, out, halves);
     return cudaGetLastError();
 }
 
 cudaError_t launch_precompute_segs(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,
-                                   int ng, const double* coef, const u64* seg, int nseg, u64 nT, TupleConst* out) {
+                                   int ng, const double* coef, const u64* seg, int nseg, u64 nT, TupleConst* out,
+                                   bool halves) {
     if (nT == 0) return cudaSuccess;
     const int threads = 128;
     u64 blocks = (nT + threads - 1) / threads;
     const u64 cap = (u64)sm_count(device) * 16;
     if (blocks > cap) blocks = cap;
-    k_tuple_precompute_segs<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, seg, nseg, nT, out);
+    k_tuple_precompute_segs<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, seg, nseg, nT, out, halves);
     return cudaGetLastError();
 }
 
