@@ -204,6 +204,12 @@ struct mist_ctx {
     mist::PinnedVec<uint64_t> cache_fp;
     uint64_t cache_key = 0;
     int cache_valid = 0;
+    // inputs of the last validated prepare() (every byte that determines the device
+    // tables) and its config count: an identical call skips re-validation
+    std::vector<unsigned char> prep_in;
+    uint64_t prep_nc = 0;
+    int prep_valid = 0;
+    mist::PinnedVec<unsigned char> prep_stage;   // page-locked staging of the uploaded tables
     // timing events (pairs)
     struct EvUse { int cat, base; bool done; };
     std::vector<cudaEvent_t> ev_pool;
