@@ -242,6 +242,28 @@ def test_retry_cache_keyed_on_groups(ctx):
     assert st == 1
 
 
+def test_prepare_cache_not_stale(ctx):
+    """prepare() skips re-validation for byte-identical inputs; any changed
+    input (here one operator-time table) must give that input's result, the
+    same as a fresh context computes."""
+    import copy
+    pb = tiny(4, 4, 1, 4, 8, 2)
+    pb2 = copy.deepcopy(pb)
+    pb2.Tf = [v * 1.5 for v in pb2.Tf]
+    s1, s2 = mist.Spec(pb), mist.Spec(pb2)
+    a1, o1, _, _ = mist.mist_pareto_frontier(ctx, s1)
+    a1b, _, _, _ = mist.mist_pareto_frontier(ctx, s1)          # cache hit
+    a2, o2, _, _ = mist.mist_pareto_frontier(ctx, s2)          # changed table
+    assert a1.tobytes() == a1b.tobytes()
+    fresh = mist.Context(0)
+    try:
+        f2, g2, _, _ = mist.mist_pareto_frontier(fresh, s2)
+    finally:
+        fresh.close()
+    assert a2.tobytes() == f2.tobytes() and np.array_equal(o2, g2)
+    assert a2.tobytes() != a1.tobytes()
+
+
 def test_eval_at_out_of_range_index(ctx):
     """Every index is range-checked on the device, at any list length: one bad
     index among 2^21 gives INVALID_ARG and the context stays usable."""
