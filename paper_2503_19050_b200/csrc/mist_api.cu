@@ -619,6 +619,7 @@ struct SweepCtx {
     bool filter = false;
     bool want_fp = false;
     u64 twin_floor = ~0ull;       // L20 twins at or above this tuple are skipped (~0: none)
+    double rate[3] = {0.0, 0.0, 0.0};   // candidates emitted per tuple, recent maximum, per mode
 };
 
 static mist_status_t read_count(mist_ctx_t* ctx, SweepCtx& S, long long* out) {
@@ -673,6 +674,21 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
         }
         return MIST_OK;
     }
+    if (!safe && S.rate[mode] > 0.0 && t_hi - t_lo > 1) {
+        // the emission rate seen so far predicts an overflow: split up front instead of
+        // rolling a whole launch back
+        const double expect = S.rate[mode] * 1.25 * (double)(t_hi - t_lo);
+        if ((double)S.count + expect > (double)(S.C / 2)) {
+            u64 piece = (u64)std::max(1.0, (double)(S.C / 4) / (S.rate[mode] * 1.25));
+            piece = std::min<u64>(piece, (t_hi - t_lo + 1) / 2);
+            for (u64 a = t_lo; a < t_hi; a += piece) {
+                mist_status_t st = eval_opt(ctx, S, mode, tuples, a, std::min<u64>(t_hi, a + piece), nv, vals,
+                                            unit_pass);
+                if (st != MIST_OK) return st;
+            }
+            return MIST_OK;
+        }
+    }
     if (!safe && S.d_fp)
         CK(cudaMemcpyAsync(S.d_fp_save, S.d_fp, sizeof(u64) * 2 * (size_t)pp.ng, cudaMemcpyDeviceToDevice,
                            ctx->stream), "save fp");
@@ -706,6 +722,10 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     long long c = 0;
     mist_status_t st = read_count(ctx, S, &c);
     if (st != MIST_OK) return st;
+    {
+        const double r = (double)(c - S.count) / (double)std::max<u64>(1, t_hi - t_lo);
+        S.rate[mode] = std::max(r, 0.5 * S.rate[mode]);   // recent maximum, decaying
+    }
     if (c <= S.C / 2) {
         S.count = c;
         return MIST_OK;
@@ -742,8 +762,21 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
         const char* e = getenv("MIST_DEDUP");
         S.twin_floor = (e && e[0] == '0') ? ~0ull : twin_floor;
     }
-    // candidate capacity: 2^26 records (2.4 GB + 1 GB sort scratch), less for small ranges
-    S.C = std::min<long long>(1LL << 26, next_pow2((long long)std::min<u64>(total_runs, 1ull << 40) * 2 + 4096));
+    // candidate capacity: up to 2^28 records (about 62 B each with the sort and bucket
+    // scratch, 17 GB), less for small ranges, and at most half of the free HBM.  A launch
+    // whose candidates would overflow half of it is rolled back and re-run in pieces,
+    // which wastes its work, so a large buffer matters on the big spaces (cfg5 at 2^26:
+    // 9 rollbacks in a one-GPU whole-space sweep).
+    S.C = std::min<long long>(1LL << 28, next_pow2((long long)std::min<u64>(total_runs, 1ull << 40) * 2 + 4096));
+    if (S.C > ctx->cand.cap) {   // only when the buffer must grow (cudaMemGetInfo is not free)
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            const long long have = std::max<long long>(ctx->cand.cap, 0);   // already held by this ctx
+            while (S.C > (1LL << 20) && S.C > have && (double)S.C * 62.0 > 0.5 * (double)fr) S.C /= 2;
+        } else {
+            cudaGetLastError();
+        }
+    }
     mist_status_t st = ensure_cand(ctx, S.C);
     if (st != MIST_OK) return st;
     S.C = ctx->cand.cap;

@@ -1465,8 +1465,17 @@ static cudaError_t launch_eval_t(cudaStream_t st, int device, const DevProblem& 
         if (e != cudaSuccess) return e;
         if (device < 64) attr_set.fetch_or(1ull << device);
     }
+    // cached occupancy query: one word (device << 40 | smem << 8 | CTAs per SM)
+    static std::atomic<unsigned long long> occ{~0ull};
+    const unsigned long long key = ((unsigned long long)(device & 0xffff) << 40) | ((unsigned long long)smem << 8);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE, NT, MINB>, NT, smem);
+    const unsigned long long w = occ.load();
+    if (w != ~0ull && (w & ~0xffull) == key) {
+        per_sm = (int)(w & 0xff);
+    } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<UNIT, MODE, NT, MINB>, NT, smem);
+        occ.store(key | (unsigned long long)(per_sm & 0xff));
+    }
     if (per_sm < 1) per_sm = 1;
     u64 blocks = (A.n_units + NT - 1) / NT;
     const u64 cap = (u64)sm_count(device) * per_sm;
@@ -1507,8 +1516,17 @@ static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& 
         if (e != cudaSuccess) return e;
         if (device < 64) attr_set.fetch_or(1ull << device);
     }
+    // cached occupancy query: one word (device << 40 | smem << 8 | CTAs per SM)
+    static std::atomic<unsigned long long> occ{~0ull};
+    const unsigned long long key = ((unsigned long long)(device & 0xffff) << 40) | ((unsigned long long)smem << 8);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW, NI>, NT, smem);
+    const unsigned long long w = occ.load();
+    if (w != ~0ull && (w & ~0xffull) == key) {
+        per_sm = (int)(w & 0xff);
+    } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW, NI>, NT, smem);
+        occ.store(key | (unsigned long long)(per_sm & 0xff));
+    }
     if (per_sm < 1) per_sm = 1;
     u64 blocks = (A.n_units + NW - 1) / NW;
     const u64 cap = (u64)sm_count(device) * per_sm;
@@ -1557,6 +1575,10 @@ static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevPr
             if (eval_cfg() == 1) {   // A/B: 3 CTAs per SM (85 registers)
                 if (!UNIT && eval_ni(P.Q)) return launch_eval_q<UNIT, 256, 3, true, 2, true>(st, device, P, A);
                 return launch_eval_q<UNIT, 256, 3, true, 2>(st, device, P, A);
+            }
+            if (eval_cfg() == 3) {   // A/B: 128-thread CTAs, 5 per SM (102 registers, 20 warps per SM)
+                if (!UNIT && eval_ni(P.Q)) return launch_eval_q<UNIT, 128, 5, true, 2, true>(st, device, P, A);
+                return launch_eval_q<UNIT, 128, 5, true, 2>(st, device, P, A);
             }
             if (!UNIT && eval_ni(P.Q)) return launch_eval_q<UNIT, 256, 2, true, 2, true>(st, device, P, A);
             return launch_eval_q<UNIT, 256, 2, true, 2>(st, device, P, A);
