@@ -620,6 +620,7 @@ struct SweepCtx {
     bool want_fp = false;
     u64 twin_floor = ~0ull;       // L20 twins at or above this tuple are skipped (~0: none)
     double rate[3] = {0.0, 0.0, 0.0};   // candidates emitted per tuple, recent maximum, per mode
+    bool rate_known[3] = {false, false, false};
 };
 
 static mist_status_t read_count(mist_ctx_t* ctx, SweepCtx& S, long long* out) {
@@ -674,6 +675,14 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
         }
         return MIST_OK;
     }
+    if (!safe && !S.rate_known[mode] && t_hi - t_lo >= (1ull << 20)) {
+        // no emission rate seen yet: a probe launch over 1/16 of the range first, so that a
+        // rollback can waste at most that much
+        const u64 probe = (t_hi - t_lo) / 16;
+        mist_status_t st = eval_opt(ctx, S, mode, tuples, t_lo, t_lo + probe, nv, vals, unit_pass);
+        if (st != MIST_OK) return st;
+        return eval_opt(ctx, S, mode, tuples, t_lo + probe, t_hi, nv, vals, unit_pass);
+    }
     if (!safe && S.rate[mode] > 0.0 && t_hi - t_lo > 1) {
         // the emission rate seen so far predicts an overflow: split up front instead of
         // rolling a whole launch back
@@ -725,6 +734,7 @@ static mist_status_t eval_opt(mist_ctx_t* ctx, SweepCtx& S, int mode, const Tupl
     {
         const double r = (double)(c - S.count) / (double)std::max<u64>(1, t_hi - t_lo);
         S.rate[mode] = std::max(r, 0.5 * S.rate[mode]);   // recent maximum, decaying
+        S.rate_known[mode] = true;
     }
     if (c <= S.C / 2) {
         S.count = c;
