@@ -309,7 +309,7 @@ def test_frontier_points_vs_oracle(ctx, seed, reduce, monkeypatch):
     sorts, the default; global radix sort + segmented scan, MIST_REDUCE=radix):
     random point sets (heavy ties in t and y, many binades, many groups, ragged
     sizes; seeds 6-8: a few groups of up to 1e5 points, so groups span many
-    2048-record chunks and several levels; seed 9: one group whose frontier alone
+    1024-record chunks and several levels; seed 9: one group whose frontier alone
     exceeds a chunk, which the bucket path hands to the radix path) equal the
     oracle's O(k^2)/sort-scan frontier of the same points, bit for bit."""
     from oracle.binding import frontier_points as orc_frontier
