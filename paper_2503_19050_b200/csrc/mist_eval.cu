@@ -11,10 +11,13 @@
 // B and B' once per run, and only the first-microbatch forward F' and the memory
 // per config.  Memory is evaluated as exact integers scaled by D = Q*TP*DP (O9),
 // so feasibility is bit-exact.  The frontier sweep (k_eval_q, CTA run queue):
-// each CTA takes a window of 256 units, one per thread for the per-unit setup;
-// the feasible runs of the window are numbered by a block prefix sum and dealt
-// to warps in batches of 32 from a shared counter.  k_eval is the
-// lockstep variant used for the dense outputs and the pilot sub-grid sweeps.
+// each CTA takes a window of 512 units, two per thread for the per-unit setup
+// (L20 twins and the tuple-level R7 cut first, then the F rows, the first
+// feasible run in closed form and the unit-level R7 cut, R7-R9); the
+// surviving runs of the window are numbered by a block prefix sum and dealt to
+// warps in batches of 32 from a shared counter.  The pilot
+// sub-grid sweep runs on the same kernel (MODE 2); k_eval is the lockstep
+// variant used for the dense outputs (and the round-1 pilot, A/B knob).
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -1027,9 +1030,10 @@ k_eval(DevProblem P, EvalArgs A) {
 // window at about the same time (less time waiting at the window barrier).
 // UPW (CTA queue only): units per thread per window; a window of NT*UPW units
 // halves the window boundaries (and their barrier tails) for UPW = 2.
-template <bool UNIT, int NT, int MINB, bool CQ, int UPW, bool NI = false>
+template <bool UNIT, int NT, int MINB, bool CQ, int UPW, bool NI = false, int MODE = 0>
 __global__ void __launch_bounds__(NT, MINB)
 k_eval_q(DevProblem P, EvalArgs A) {
+    static_assert(MODE == 0 || (MODE == 2 && CQ), "the pilot sub-grid (MODE 2) runs on the CTA queue");
     static_assert(CQ || UPW == 1, "several units per thread need the CTA queue");
     constexpr int NW = NT * UPW;                                     // units per window
     static_assert(sizeof(TupleConst) % 16 == 0, "bulk copies move whole tuples in 16-byte units");
@@ -1053,7 +1057,9 @@ k_eval_q(DevProblem P, EvalArgs A) {
     const int Q1 = P.Q1;
     const unsigned lane = tid & 31;
     UnitState* wU = sU + (tid & ~31);
-    const unsigned radix = (unsigned)Q1;
+    // MODE 2 (pilot): ratio indices address the sub-grid values vals[0..nv) on every axis
+    const unsigned radix = MODE == 2 ? A.nv : (unsigned)Q1;
+    auto val = [&](unsigned i) -> unsigned { return MODE == 2 ? A.vals[i] : i; };
     const unsigned upt = A.upt;
     const u64 n_units = A.n_units;
     unsigned nph = 0, nlb = 0;
@@ -1132,7 +1138,9 @@ k_eval_q(DevProblem P, EvalArgs A) {
             unsigned kWj = (unsigned)((float)jj * inv_rad);
             kWj -= kWj * radix > jj ? 1u : 0u;
             kWj += (kWj + 1u) * radix <= jj ? 1u : 0u;
-            const unsigned kAj = jj - kWj * radix;
+            const unsigned iAj = jj - kWj * radix;
+            kWj = val(jj < radix * radix ? kWj : 0u);               // ratio values (MODE 2: sub-grid)
+            const unsigned kAj = val(jj < radix * radix ? iAj : 0u);
             bool active = u < n_units && jj < radix * radix && kWj <= (unsigned)P.kmax[0] &&
                           kAj <= (unsigned)P.kmax[3];                    // preset ranges
             if (active && sT[tkj].twin_T >= A.twin_floor && sT[tkj].twin_T != ~0ull) active = false;   // L20 twin
@@ -1142,7 +1150,12 @@ k_eval_q(DevProblem P, EvalArgs A) {
                 active = false;
                 MIST_CTR(4, (unsigned)P.kmax[1] + 1u);
             }
-            const unsigned gend = (unsigned)P.kmax[1] + 1u;              // runs kG < gend
+            // runs: kG indices [0, gend) (MODE 2: the sub-grid values within the preset range)
+            unsigned gend = (unsigned)P.kmax[1] + 1u;
+            if (MODE == 2) {
+                gend = 0;
+                while (gend < radix && A.vals[gend] <= (unsigned)P.kmax[1]) ++gend;
+            }
             unsigned g0j = radix, g1j = gend;
             {
                 const TupleConst& tc = sT[tkj];
@@ -1152,7 +1165,16 @@ k_eval_q(DevProblem P, EvalArgs A) {
                     sU[w] = us;
                     nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
                            (unsigned)(tc.last != 0);
-                    if (tc.mG >= tc.gb_k) {
+                    if (MODE == 2) {
+                        // sub-grid: scan its few kG values at the last admitted kO value
+                        const double kOv = (double)A.vals[(P.kmax[2] == P.Q ? radix : 1u) - 1u];
+                        RunState rm;
+                        for (unsigned ig = 0; ig < gend; ++ig) {
+                            run_memory(tc, (double)kWj, (double)A.vals[ig], (double)kAj, Q, rm);
+                            if (mem_kO(tc, rm, kOv, Q) <= tc.DMB) { g0j = ig; break; }
+                        }
+                        if (!(tc.mG >= tc.gb_k)) g0j = 0;
+                    } else if (tc.mG >= tc.gb_k) {
 #ifdef MIST_G0_SCAN
                         RunState rm;
                         for (unsigned ig = 0; ig < gend; ++ig) {
@@ -1171,7 +1193,7 @@ k_eval_q(DevProblem P, EvalArgs A) {
                     // fingerprints, which count every feasible config)
                     if (r7 && g0j < gend) {
                         g1j = run_cut<UNIT, NI>(P, tc, us, kWj, kAj, g0j, gend, FG, fv.t, fv.y, fv.off[tc.group],
-                                                fv.off[tc.group + 1], nlb);
+                                                fv.off[tc.group + 1], nlb, MODE == 2 ? A.vals : nullptr);
                         MIST_CTR(4, gend - g1j);
                     }
                 }
@@ -1259,13 +1281,13 @@ k_eval_q(DevProblem P, EvalArgs A) {
             if (r < total) {
                 const TupleConst& tc = sT[o_tk];
                 const unsigned grp = tc.group;
-                const unsigned kG = o_g0 + (r - o_ex);
+                const unsigned kG = val(o_g0 + (r - o_ex));
                 const unsigned nrows = (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) +
                                        (unsigned)(tc.first != 0) + (unsigned)(tc.last != 0);
                 const unsigned brows = nrows * (tc.L.N_Bp != tc.L.N_B ? 2u : 1u);
                 const bool same = cv && cgrp == grp;
                 u64 fcnt = 0, fhash = 0;
-                const RunCand rc = frontier_run<UNIT, 0, NI>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
+                const RunCand rc = frontier_run<UNIT, MODE, NI>(P, A, tc, ou, o_kW, kG, o_kA, radix, Q, Q1, grp, FG, same,
                                                          ct, cy, nrows, brows, nph, nlb, fcnt, fhash, fv, ctr);
                 if (A.fp && fcnt) {
                     atomicAdd(A.fp + 2 * (u64)grp, fcnt);
@@ -1501,7 +1523,7 @@ static int eval_cfg() {
     return v;
 }
 
-template <bool UNIT, int NT, int MINB, bool CQ, int UPW = 1, bool NI = false>
+template <bool UNIT, int NT, int MINB, bool CQ, int UPW = 1, bool NI = false, int MODE = 0>
 static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     constexpr size_t NW = (size_t)NT * UPW;
     const size_t maxt = (NW + A.upt - 1) / A.upt + 1;
@@ -1511,7 +1533,7 @@ static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& 
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     static std::atomic<unsigned long long> attr_set{0};   // the attribute is per device: one bit per device
     if (device >= 64 || !((attr_set.load() >> device) & 1ull)) {
-        cudaError_t e = cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ, UPW, NI>,
+        cudaError_t e = cudaFuncSetAttribute(k_eval_q<UNIT, NT, MINB, CQ, UPW, NI, MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
         if (device < 64) attr_set.fetch_or(1ull << device);
@@ -1524,7 +1546,7 @@ static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& 
     if (w != ~0ull && (w & ~0xffull) == key) {
         per_sm = (int)(w & 0xff);
     } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW, NI>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_q<UNIT, NT, MINB, CQ, UPW, NI, MODE>, NT, smem);
         occ.store(key | (unsigned long long)(per_sm & 0xff));
     }
     if (per_sm < 1) per_sm = 1;
@@ -1532,7 +1554,7 @@ static cudaError_t launch_eval_q(cudaStream_t st, int device, const DevProblem& 
     const u64 cap = (u64)sm_count(device) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) return cudaSuccess;
-    k_eval_q<UNIT, NT, MINB, CQ, UPW, NI><<<(unsigned)blocks, NT, smem, st>>>(P, A);
+    k_eval_q<UNIT, NT, MINB, CQ, UPW, NI, MODE><<<(unsigned)blocks, NT, smem, st>>>(P, A);
     return cudaGetLastError();
 }
 
@@ -1603,14 +1625,30 @@ static cudaError_t launch_frontier_eval(cudaStream_t st, int device, const DevPr
     }
 }
 
+// The pilot sub-grid sweep (MODE 2): the CTA run queue by default (windows of 256
+// units); MIST_PILOT_KERNEL=lockstep selects the round-1 lockstep kernel.
+static bool pilot_queue() {
+    const char* s = getenv("MIST_PILOT_KERNEL");
+    return !(s && !strcmp(s, "lockstep"));
+}
+
 cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A, int mode) {
     if (P.unit_factors) {
         if (mode == 1) return launch_eval_t<true, 1, 256, 2>(st, device, P, A);
-        if (mode == 2) return launch_eval_t<true, 2, 256, 2>(st, device, P, A);
+        if (mode == 2) {
+            if (pilot_queue()) return launch_eval_q<true, 256, 2, true, 1, false, 2>(st, device, P, A);
+            return launch_eval_t<true, 2, 256, 2>(st, device, P, A);
+        }
         return launch_frontier_eval<true>(st, device, P, A);
     }
     if (mode == 1) return launch_eval_t<false, 1, 256, 2>(st, device, P, A);
-    if (mode == 2) return launch_eval_t<false, 2, 256, 2>(st, device, P, A);
+    if (mode == 2) {
+        if (pilot_queue()) {
+            if (eval_ni(P.Q)) return launch_eval_q<false, 256, 2, true, 1, true, 2>(st, device, P, A);
+            return launch_eval_q<false, 256, 2, true, 1, false, 2>(st, device, P, A);
+        }
+        return launch_eval_t<false, 2, 256, 2>(st, device, P, A);
+    }
     return launch_frontier_eval<false>(st, device, P, A);
 }
 
