@@ -12,7 +12,7 @@ for w in 3 4; do timeout 600 python tools/prof_step.py --workload $w --warmup 1 
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 CMD="python tools/prof_step.py --workload 2 --warmup 0 --steps 1"
 MIST_COUNTERS=1 timeout 300 python tools/prof_step.py --workload 5 --start 0.5 --fraction 0.005 --warmup 0 --steps 1 > gpurun_out/ctr_${TAG}_c5w.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_eval_q -c 1 -o gpurun_out/prof_eval_$TAG $CMD > gpurun_out/ncu_eval_$TAG.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_eval_q --launch-skip 1 -c 1 -o gpurun_out/prof_eval_$TAG $CMD > gpurun_out/ncu_eval_$TAG.log 2>&1
 ncu -i gpurun_out/prof_eval_$TAG.ncu-rep --page raw --csv > gpurun_out/prof_eval_${TAG}_raw.csv 2>/dev/null
 ncu -i gpurun_out/prof_eval_$TAG.ncu-rep --page details --csv > gpurun_out/prof_eval_${TAG}_details.csv 2>/dev/null
 ncu -i gpurun_out/prof_eval_$TAG.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/prof_eval_${TAG}_source.csv 2>/dev/null
