@@ -1362,6 +1362,25 @@ k_pilot_zero(DevProblem P, EvalArgs A) {
                     run_memory(tc, 0.0, 0.0, (double)kA, Q, rs);
                     const double memD = mem_kO(tc, rs, 0.0, Q);
                     if (!(memD <= tc.DMB)) continue;           // Eq. 4
+                    if (has) {
+                        // R4 bound of t at this kA (channels at kW = kG = 0): skip the rows when
+                        // even the bound cannot beat the best t found (the smaller kA stays on ties)
+                        const double dkA = kA;
+                        double lb = 0.0;
+                        if (tc.nl0 > 0.0)
+                            lb += tc.nl0 * (dmax(dmax(tc.L.C_F, tc.L.N_F), dkA * tc.L.sAd) +
+                                            dmax(dmax(tc.L.C_B, tc.L.N_B), dkA * tc.L.sAh));
+                        if (tc.nl1 > 0.0)
+                            lb += tc.nl1 * (dmax(dmax(tc.L.C_F, tc.L.N_F), dkA * tc.L.sAd1) +
+                                            dmax(dmax(tc.L.C_B1, tc.L.N_B), dkA * tc.L.sAh1));
+                        if (tc.first)
+                            lb += dmax(dmax(tc.E.C_F, tc.E.N_F), dkA * tc.E.sAd) +
+                                  dmax(dmax(tc.E.C_B, tc.E.N_B), dkA * tc.E.sAh);
+                        if (tc.last)
+                            lb += dmax(dmax(tc.H.C_F, tc.H.N_F), dkA * tc.H.sAd) +
+                                  dmax(dmax(tc.H.C_B, tc.H.N_B), dkA * tc.H.sAh);
+                        if ((lb + tc.t_p2p) * (1.0 - 1e-12) >= bt) continue;
+                    }
                     UnitState us;
                     unit_forward<UNIT>(tc, 0.0, (double)kA, FG, us);
                     run_backward<UNIT>(tc, us, 0.0, 0.0, (double)kA, FG, rs);

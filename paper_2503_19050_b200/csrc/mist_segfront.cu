@@ -88,16 +88,6 @@ __device__ __forceinline__ bool lex_less(double ta, double ya, u64 ia, double tb
     return ta < tb || (ta == tb && (ya < yb || (ya == yb && ia < ib)));
 }
 
-// group of chunk c: the last g with co[g] <= c (co = exclusive scan of chunks per group)
-__device__ __forceinline__ int chunk_group(const u32* __restrict__ co, int ng, u32 c) {
-    int lo = 0, hi = ng - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (co[mid] <= c) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
 __device__ __forceinline__ u32 block_excl_count(u32 mine, u32* s_wcnt, u32& all) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     u32 pre = mine;
@@ -125,7 +115,8 @@ __device__ __forceinline__ u32 block_excl_count(u32 mine, u32* s_wcnt, u32& all)
 // that another of its 8 beats (O10, pairwise), so only the survivors are sorted.
 __global__ void __launch_bounds__(kChunkThreads)
 k_chunk_front(CandBuf X, const u32* __restrict__ cnt, const u32* __restrict__ goff, const u32* __restrict__ co,
-              int ng, const u32* __restrict__ nchunks, u32* __restrict__ nf) {
+              const u32* __restrict__ cmap, const u32* __restrict__ fin, const u32* __restrict__ nchunks,
+              u32* __restrict__ nf) {
     extern __shared__ __align__(16) double s_t[];     // [kChunk + 1] t, then y, idx; permutation [kChunk]
     double* s_y = s_t + (kChunk + 1);
     u64* s_i = reinterpret_cast<u64*>(s_y + (kChunk + 1));
@@ -137,10 +128,14 @@ k_chunk_front(CandBuf X, const u32* __restrict__ cnt, const u32* __restrict__ go
     if (blockIdx.x == 0 && tid == 0) nf[total] = 0;      // the scan runs over total + 1 entries
     if (tid == 0) { s_t[kChunk] = CUDART_INF; s_y[kChunk] = CUDART_INF; s_i[kChunk] = ~0ull; }   // sentinel
     for (u32 c = blockIdx.x; c < total; c += gridDim.x) {
-        const int g = chunk_group(co, ng, c);
+        const int g = (int)cmap[c];
         const u32 j = c - co[g];
         const u32 start = goff[g] + j * kChunk;
         const int len = (int)min((u32)kChunk, cnt[g] - j * kChunk);
+        if (fin[g]) {                                     // already a final, sorted frontier
+            if (tid == 0) nf[c] = (u32)len;
+            continue;
+        }
         __syncthreads();                                  // previous chunk done with smem
         for (int k = tid; k < len; k += kChunkThreads) {
             s_t[k] = X.t[start + k]; s_y[k] = X.y[start + k]; s_i[k] = X.idx[start + k];
@@ -238,12 +233,12 @@ k_chunk_front(CandBuf X, const u32* __restrict__ cnt, const u32* __restrict__ go
 }
 
 // chunk c's nf[c] frontier records -> Y[out[c], +nf[c]) (out = exclusive scan of nf)
-__global__ void k_chunk_compact(CandBuf X, const u32* __restrict__ goff, const u32* __restrict__ co, int ng,
-                                const u32* __restrict__ nchunks, const u32* __restrict__ nf,
-                                const u32* __restrict__ out, CandBuf Y) {
+__global__ void k_chunk_compact(CandBuf X, const u32* __restrict__ goff, const u32* __restrict__ co,
+                                const u32* __restrict__ cmap, const u32* __restrict__ nchunks,
+                                const u32* __restrict__ nf, const u32* __restrict__ out, CandBuf Y) {
     const u32 total = *nchunks;
     for (u32 c = blockIdx.x; c < total; c += gridDim.x) {
-        const int g = chunk_group(co, ng, c);
+        const int g = (int)cmap[c];
         const u32 start = goff[g] + (c - co[g]) * kChunk, n = nf[c], o = out[c];
         for (u32 k = threadIdx.x; k < n; k += blockDim.x) {
             Y.t[o + k] = X.t[start + k]; Y.y[o + k] = X.y[start + k]; Y.mem[o + k] = X.mem[start + k];
@@ -252,13 +247,23 @@ __global__ void k_chunk_compact(CandBuf X, const u32* __restrict__ goff, const u
     }
 }
 
+// chunk -> group map (one thread per group writes its chunks), so a chunk's CTA reads
+// its group with one load instead of a binary search over the chunk offsets
+__global__ void k_seg_chunk_map(const u32* __restrict__ co, int ng, u32* __restrict__ cmap) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x)
+        for (u32 c = co[g]; c < co[g + 1]; ++c) cmap[c] = (u32)g;
+}
+
 // next level's per-group counts and offsets from the packed chunk frontiers
+// A group that fitted one chunk at this level already holds its final frontier,
+// sorted (fin[g] = 1): later levels only carry it along.
 __global__ void k_seg_regroup(const u32* __restrict__ co, int ng, const u32* __restrict__ out, u32* __restrict__ cnt,
-                              u32* __restrict__ goff) {
+                              u32* __restrict__ goff, u32* __restrict__ fin) {
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
         const u32 a = out[co[g]], b = out[co[g + 1]];
         cnt[g] = b - a;
         goff[g] = a;
+        if (co[g + 1] - co[g] == 1) fin[g] = 1u;
     }
 }
 
@@ -280,7 +285,7 @@ static unsigned grid_n(long long n, int threads, int cap = 148 * 8) {
 // device words, scan tiles.
 long long seg_scratch_words(long long n, long long ng) {
     const long long nch = n / kChunk + ng + 2;
-    return n + 4 * (ng + 2) + 2 * (nch + 1) + 8 + 2 * scan_tmp_words(std::max(nch, ng + 1)) + 64;
+    return n + 5 * (ng + 2) + 3 * (nch + 1) + 8 + 2 * scan_tmp_words(std::max(nch, ng + 1)) + 64;
 }
 
 cudaError_t frontier_reduce_seg(cudaStream_t st, CandBuf cand, long long n, int ng, u32* ws, long long ws_words,
@@ -297,13 +302,17 @@ cudaError_t frontier_reduce_seg(cudaStream_t st, CandBuf cand, long long n, int 
     u32* co = cpg + (ng + 2);
     u32* nf = co + (ng + 2);
     u32* out = nf + (nch_max + 1);
-    u32* dev = out + (nch_max + 1);              // [0] nchunks, [1] multi, [2] total
+    u32* cmap = out + (nch_max + 1);             // chunk -> group
+    u32* fin = cmap + (nch_max + 1);             // group already final (one chunk at a previous level)
+    u32* dev = fin + (ng + 2);                   // [0] nchunks, [1] multi, [2] total
     u32* stmp = dev + 8;
     CandBuf A = cand, B = cand;                   // A = [0, n), B = [n, 2n)
     B.t += n; B.y += n; B.mem += n; B.idx += n; B.group += n;
     const int T = 256;
     // level 0: bucket by group
     err = cudaMemsetAsync(cnt, 0, sizeof(u32) * (size_t)ng, st);
+    if (err != cudaSuccess) return err;
+    err = cudaMemsetAsync(fin, 0, sizeof(u32) * (size_t)ng, st);
     if (err != cudaSuccess) return err;
     k_seg_count<<<grid_n(n, T), T, 0, st>>>(A.group, n, cnt, rank);
     err = scan_u32_exclusive(st, cnt, goff, ng, stmp, nullptr);
@@ -339,10 +348,11 @@ cudaError_t frontier_reduce_seg(cudaStream_t st, CandBuf cand, long long n, int 
         err = scan_u32_exclusive(st, cpg, co, ng + 1, stmp, dev);    // co[ng] = chunks, dev[0] = chunks
         if (err != cudaSuccess) return err;
         const unsigned grid = (unsigned)std::min<long long>(nch_bound, cta);
-        k_chunk_front<<<grid, kChunkThreads, kChunkSmem, st>>>(X, cnt, goff, co, ng, dev, nf);
+        k_seg_chunk_map<<<grid_n(ng, T), T, 0, st>>>(co, ng, cmap);
+        k_chunk_front<<<grid, kChunkThreads, kChunkSmem, st>>>(X, cnt, goff, co, cmap, fin, dev, nf);
         err = scan_u32_exclusive(st, nf, out, nch_bound + 1, stmp, dev + 2);
         if (err != cudaSuccess) return err;
-        k_chunk_compact<<<grid, 128, 0, st>>>(X, goff, co, ng, dev, nf, out, Y);
+        k_chunk_compact<<<grid, 128, 0, st>>>(X, goff, co, cmap, dev, nf, out, Y);
         rs->launches += 8;
         rs->passes++;
         u32 h[3] = {0, 0, 0};
@@ -359,7 +369,7 @@ cudaError_t frontier_reduce_seg(cudaStream_t st, CandBuf cand, long long n, int 
             *n_out = tot;
             return cudaGetLastError();
         }
-        k_seg_regroup<<<grid_n(ng, T), T, 0, st>>>(co, ng, out, cnt, goff);
+        k_seg_regroup<<<grid_n(ng, T), T, 0, st>>>(co, ng, out, cnt, goff, fin);
         rs->launches++;
         n_cur = h[2];
         std::swap(X, Y);
