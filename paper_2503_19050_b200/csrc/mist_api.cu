@@ -1129,11 +1129,23 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         ev_end(ctx, htot);
         ctx->stats.d2h_bytes = sizeof(mist_point_t) * (uint64_t)nf + sizeof(int64_t) * ((uint64_t)pp.ng + 1) +
                                (want_fp ? sizeof(u64) * 2 * (uint64_t)pp.ng : 0);
-        CK(ctx->cache_points.resize((size_t)nf), "pinned points");
+        // The caller's buffers fit: the frontier goes straight to them (one copy, any memory
+        // kind).  Else it goes to the page-locked cache that serves the BUFFER_TOO_SMALL retry.
+        const bool direct = out && out_cap >= nf;
         CK(ctx->cache_offsets.resize((size_t)pp.ng + 1), "pinned offsets");
-        if (nf > 0)
-            CK(cudaMemcpyAsync(ctx->cache_points.data(), d_pts, sizeof(mist_point_t) * (size_t)nf,
-                               cudaMemcpyDeviceToHost, ctx->stream), "D2H points");
+        if (direct) {
+            ctx->cache_points.resize(0);
+            if (nf > 0)
+                CK(cudaMemcpyAsync(out, d_pts, sizeof(mist_point_t) * (size_t)nf, cudaMemcpyDefault, ctx->stream),
+                   "D2H points");
+        } else {
+            CK(ctx->cache_points.resize((size_t)nf), "pinned points");
+            if (nf > 0)
+                CK(cudaMemcpyAsync(ctx->cache_points.data(), d_pts, sizeof(mist_point_t) * (size_t)nf,
+                                   cudaMemcpyDeviceToHost, ctx->stream), "D2H points");
+        }
+        ctx->cache_nf = nf;
+        ctx->cache_direct = direct;
         CK(cudaMemcpyAsync(ctx->cache_offsets.data(), d_off, sizeof(int64_t) * ((size_t)pp.ng + 1),
                            cudaMemcpyDeviceToHost, ctx->stream), "D2H offsets");
         if (want_fp) {
@@ -1144,13 +1156,16 @@ extern "C" mist_status_t mist_pareto_frontier(mist_ctx_t* ctx, const mist_model_
         CK(cudaStreamSynchronize(ctx->stream), "final sync");
         ev_flush(ctx);
         ctx->cache_key = key;
-        ctx->cache_valid = 1;
+        ctx->cache_valid = ctx->cache_direct ? 0 : 1;   // a direct call has delivered its points
+    } else {
+        ctx->cache_direct = false;
     }
-    const int64_t nf = (int64_t)ctx->cache_points.size();
+    const int64_t nf = ctx->cache_nf;
     *n_out = nf;
     if (out_cap < nf || (!out && nf > 0)) return fail(ctx, MIST_ERR_BUFFER_TOO_SMALL, "out_cap too small");
     const size_t ng = ctx->cache_offsets.size() - 1;
-    if (nf > 0) CK(cudaMemcpy(out, ctx->cache_points.data(), sizeof(mist_point_t) * (size_t)nf, cudaMemcpyDefault), "copy out");
+    if (nf > 0 && !ctx->cache_direct)
+        CK(cudaMemcpy(out, ctx->cache_points.data(), sizeof(mist_point_t) * (size_t)nf, cudaMemcpyDefault), "copy out");
     if (group_offsets)
         CK(cudaMemcpy(group_offsets, ctx->cache_offsets.data(), sizeof(int64_t) * (ng + 1), cudaMemcpyDefault), "copy offsets");
     if (want_fp) {

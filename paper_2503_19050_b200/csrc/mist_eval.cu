@@ -1452,11 +1452,14 @@ __global__ void k_eval_at(DevProblem P, const DevGroup* __restrict__ groups, int
 // host launchers
 // ---------------------------------------------------------------------------
 static int sm_count(int device) {
-    static int cached[64] = {0};
-    if (device < 64 && cached[device]) return cached[device];
+    static std::atomic<int> cached[64];   // zero-initialised (static storage)
+    if (device >= 0 && device < 64) {
+        const int c = cached[device].load();
+        if (c) return c;
+    }
     int n = 148;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
-    if (device < 64) cached[device] = n;
+    if (device >= 0 && device < 64) cached[device].store(n);
     return n;
 }
 

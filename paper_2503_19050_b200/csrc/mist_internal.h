@@ -204,6 +204,8 @@ struct mist_ctx {
     mist::PinnedVec<uint64_t> cache_fp;
     uint64_t cache_key = 0;
     int cache_valid = 0;
+    int64_t cache_nf = 0;          // frontier points of the last computed call
+    bool cache_direct = false;     // the last computed call wrote its points to the caller directly
     // inputs of the last validated prepare() (every byte that determines the device
     // tables) and its config count: an identical call skips re-validation
     std::vector<unsigned char> prep_in;
