@@ -644,6 +644,45 @@ __device__ MIST_CUT_ATTR unsigned run_cut(const DevProblem& P, const TupleConst&
     return b;
 }
 
+// Quick form of R7's unit cut before the unit's F rows exist: every config of the
+// unit's runs kG >= g0 has t >= sum count (R4(F at kW, kA) + lb(B at g0)) + p2p, with
+// R4(F) = the max of F's channels <= T(F) (factors >= 1).  True when the group's y = 0
+// staircase point lies strictly left of that bound (then every run of the unit is
+// beaten, O10); the exact cut with T(F) follows otherwise.
+template <bool UNIT, bool NI>
+__device__ __forceinline__ bool unit_quick_cut(const TupleConst& tc, double kW, double kA, double kG0,
+                                               const FGRow* FG, const double* ft, const double* fy, long long lo,
+                                               long long hi, unsigned& nlb) {
+    if (lo >= hi || !(fy[hi - 1] <= 0.0)) return false;
+    const double FHL = kW * tc.L.sWh;
+    double lb = 0.0;
+    unsigned rows = 0;
+    if (tc.nl0 > 0.0) {
+        lb += tc.nl0 * (dmax(dmax(tc.L.C_F, tc.L.N_F), dmax(FHL, kA * tc.L.sAd)) +
+                        lb_backward<UNIT, NI>(tc.L, false, FHL, kG0, kA, FG));
+        ++rows;
+    }
+    if (tc.nl1 > 0.0) {
+        lb += tc.nl1 * (dmax(dmax(tc.L.C_F, tc.L.N_F), dmax(FHL, kA * tc.L.sAd1)) +
+                        lb_backward<UNIT, NI>(tc.L, true, FHL, kG0, kA, FG));
+        ++rows;
+    }
+    if (tc.first) {
+        const double FHE = kW * tc.E.sWh;
+        lb += dmax(dmax(tc.E.C_F, tc.E.N_F), dmax(FHE, kA * tc.E.sAd)) +
+              lb_backward<UNIT, NI>(tc.E, false, FHE, kG0, kA, FG);
+        ++rows;
+    }
+    if (tc.last) {
+        const double FHH = kW * tc.H.sWh;
+        lb += dmax(dmax(tc.H.C_F, tc.H.N_F), dmax(FHH, kA * tc.H.sAd)) +
+              lb_backward<UNIT, NI>(tc.H, false, FHH, kG0, kA, FG);
+        ++rows;
+    }
+    if (kG0 != 0.0) nlb += rows;
+    return ft[hi - 1] < (lb + tc.t_p2p) * (1.0 - 1e-12);
+}
+
 // fill the {f, g} factor table (non-members: f = 1, g = 0)
 __device__ __forceinline__ void load_fg(const DevProblem& P, FGRow* FG, int tid) {
     if (tid < 64) {
@@ -1160,11 +1199,6 @@ k_eval_q(DevProblem P, EvalArgs A) {
             {
                 const TupleConst& tc = sT[tkj];
                 if (active) {
-                    UnitState us;
-                    unit_forward<UNIT>(tc, (double)kWj, (double)kAj, FG, us);
-                    sU[w] = us;
-                    nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
-                           (unsigned)(tc.last != 0);
                     if (MODE == 2) {
                         // sub-grid: scan its few kG values at the last admitted kO value
                         const double kOv = (double)A.vals[(P.kmax[2] == P.Q ? radix : 1u) - 1u];
@@ -1189,12 +1223,32 @@ k_eval_q(DevProblem P, EvalArgs A) {
                     } else {
                         g0j = 0;                       // no kG-suffix property: every run is a task
                     }
-                    // R7: runs the staircase beats on t alone are never dealt (not with
-                    // fingerprints, which count every feasible config)
-                    if (r7 && g0j < gend) {
-                        g1j = run_cut<UNIT, NI>(P, tc, us, kWj, kAj, g0j, gend, FG, fv.t, fv.y, fv.off[tc.group],
-                                                fv.off[tc.group + 1], nlb, MODE == 2 ? A.vals : nullptr);
-                        MIST_CTR(4, gend - g1j);
+                    // A unit without a feasible run, or whose first run a cheap bound (R4 rows of
+                    // F in place of the exact ones, R7) already puts past the y = 0 staircase
+                    // point, needs no F rows at all.  The cheap bound pays on the long kO axes
+                    // only (same-box A/B: cfg3 Q = 20 and cfg5 Q = 50 1-2% faster, cfg2 Q = 10
+                    // and cfg4 Q = 8 1-2% slower, profiles/r2/ab_quick_cut_summary.txt).
+                    if (g0j < gend && r7 && !P.ykey && P.Q >= 16 &&
+                        unit_quick_cut<UNIT, NI>(tc, (double)kWj, (double)kAj,
+                                                 (double)(MODE == 2 ? A.vals[g0j] : g0j), FG, fv.t, fv.y,
+                                                 fv.off[tc.group], fv.off[tc.group + 1], nlb)) {
+                        g1j = g0j;
+                        MIST_CTR(4, gend - g0j);
+                    }
+                    if (g0j < g1j) {
+                        UnitState us;
+                        unit_forward<UNIT>(tc, (double)kWj, (double)kAj, FG, us);
+                        sU[w] = us;
+                        nph += (unsigned)(tc.nl0 > 0.0) + (unsigned)(tc.nl1 > 0.0) + (unsigned)(tc.first != 0) +
+                               (unsigned)(tc.last != 0);
+                        // R7: runs the staircase beats on t alone are never dealt (not with
+                        // fingerprints, which count every feasible config)
+                        if (r7) {
+                            g1j = run_cut<UNIT, NI>(P, tc, us, kWj, kAj, g0j, gend, FG, fv.t, fv.y,
+                                                    fv.off[tc.group], fv.off[tc.group + 1], nlb,
+                                                    MODE == 2 ? A.vals : nullptr);
+                            MIST_CTR(4, gend - g1j);
+                        }
                     }
                 }
             }
