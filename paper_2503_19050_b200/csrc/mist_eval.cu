@@ -160,29 +160,51 @@ __device__ __forceinline__ u64 half_order(u64 i, u64 nT, bool halves) {
     return i < h ? 2 * i : 2 * (i - h) + 1;
 }
 
-__global__ void k_tuple_precompute_segs(DevProblem P, const DevGroup* __restrict__ groups, int ng,
-                                        const double* __restrict__ coef, const u64* __restrict__ seg, int nseg,
-                                        u64 nT, TupleConst* __restrict__ out, bool halves) {
-    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < nT; o += (u64)gridDim.x * blockDim.x) {
-        const u64 i = half_order(o, nT, halves);
-        int lo = 0, hi = nseg - 1;                  // last segment whose first position <= i
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (seg[2 * mid + 1] <= i) lo = mid; else hi = mid - 1;
+// Both precompute kernels run kPreThreads threads per CTA: every thread builds its
+// tuple into shared memory and the CTA then writes its tuples out as one contiguous,
+// coalesced stream (a per-thread struct store would touch 72 separate 576-B-strided
+// words per warp instruction).
+constexpr int kPreThreads = 64;
+
+__device__ __forceinline__ void store_tuples(TupleConst* sT, u64 o0, u64 nT, TupleConst* __restrict__ out) {
+    __syncthreads();
+    const int nt = (int)min((u64)kPreThreads, nT - o0);
+    const double2* src = reinterpret_cast<const double2*>(sT);
+    double2* dst = reinterpret_cast<double2*>(out + o0);
+    const int nw = nt * (int)(sizeof(TupleConst) / 16);
+    for (int i = threadIdx.x; i < nw; i += kPreThreads) dst[i] = src[i];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPreThreads)
+k_tuple_precompute_segs(DevProblem P, const DevGroup* __restrict__ groups, int ng,
+                        const double* __restrict__ coef, const u64* __restrict__ seg, int nseg,
+                        u64 nT, TupleConst* __restrict__ out, bool halves) {
+    __shared__ __align__(16) TupleConst sT[kPreThreads];
+    for (u64 o0 = (u64)blockIdx.x * kPreThreads; o0 < nT; o0 += (u64)gridDim.x * kPreThreads) {
+        const u64 o = o0 + threadIdx.x;
+        if (o < nT) {
+            const u64 i = half_order(o, nT, halves);
+            int lo = 0, hi = nseg - 1;              // last segment whose first position <= i
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (seg[2 * mid + 1] <= i) lo = mid; else hi = mid - 1;
+            }
+            make_tuple(P, groups, ng, coef, seg[2 * lo] + (i - seg[2 * lo + 1]), sT[threadIdx.x]);
         }
-        TupleConst tc;
-        make_tuple(P, groups, ng, coef, seg[2 * lo] + (i - seg[2 * lo + 1]), tc);
-        out[o] = tc;
+        store_tuples(sT, o0, nT, out);
     }
 }
 
-__global__ void k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ groups, int ng,
-                                   const double* __restrict__ coef, u64 T0, u64 nT,
-                                   TupleConst* __restrict__ out, bool halves) {
-    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < nT; o += (u64)gridDim.x * blockDim.x) {
-        TupleConst tc;
-        make_tuple(P, groups, ng, coef, T0 + half_order(o, nT, halves), tc);
-        out[o] = tc;
+__global__ void __launch_bounds__(kPreThreads)
+k_tuple_precompute(DevProblem P, const DevGroup* __restrict__ groups, int ng,
+                   const double* __restrict__ coef, u64 T0, u64 nT,
+                   TupleConst* __restrict__ out, bool halves) {
+    __shared__ __align__(16) TupleConst sT[kPreThreads];
+    for (u64 o0 = (u64)blockIdx.x * kPreThreads; o0 < nT; o0 += (u64)gridDim.x * kPreThreads) {
+        const u64 o = o0 + threadIdx.x;
+        if (o < nT) make_tuple(P, groups, ng, coef, T0 + half_order(o, nT, halves), sT[threadIdx.x]);
+        store_tuples(sT, o0, nT, out);
     }
 }
 
@@ -1387,23 +1409,32 @@ k_eval_q(DevProblem P, EvalArgs A) {
 // lanes).  The candidates are real feasible configs, so any point they beat is
 // beaten (O10): the staircase they join stays exact.
 template <bool UNIT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(64)
 k_pilot_zero(DevProblem P, EvalArgs A) {
+    constexpr int NT = 64;                                  // launched with NT threads
     __shared__ FGRow FG[16];
+    __shared__ __align__(16) TupleConst sT[NT];             // the CTA's tuples, loaded coalesced
     load_fg(P, FG, threadIdx.x);
-    __syncthreads();
     const double Q = P.Q;
     const unsigned lane = threadIdx.x & 31;
     const u64 nT = A.n_units;
-    for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < nT;
-         base += (u64)gridDim.x * blockDim.x) {
-        const u64 T = base + lane;
+    for (u64 base = (u64)blockIdx.x * NT; base < nT; base += (u64)gridDim.x * NT) {
+        __syncthreads();                                    // previous window done with sT
+        {
+            const int nt = (int)min((u64)NT, nT - base);
+            const double* src = reinterpret_cast<const double*>(A.tuples + base);
+            double* dst = reinterpret_cast<double*>(sT);
+            const int nw = nt * (int)(sizeof(TupleConst) / 8);
+            for (int i = threadIdx.x; i < nw; i += NT) dst[i] = __ldg(src + i);
+        }
+        __syncthreads();
+        const u64 T = base + threadIdx.x;
         bool has = false;
         double bt = CUDART_INF, bm = 0.0;
         u64 bi = 0;
         unsigned grp = 0xffffffffu;
         if (T < nT) {
-            const TupleConst& tc = A.tuples[T];
+            const TupleConst& tc = sT[threadIdx.x];
             grp = (unsigned)tc.group;
             const bool bp_eq = tc.L.N_Bp == tc.L.N_B && (!tc.first || tc.E.N_Bp == tc.E.N_B) &&
                                (!tc.last || tc.H.N_Bp == tc.H.N_B);
@@ -1520,9 +1551,9 @@ static int sm_count(int device) {
 cudaError_t launch_precompute(cudaStream_t st, int device, const DevProblem& P, const DevGroup* groups,
                               int ng, const double* coef, u64 T0, u64 nT, TupleConst* out, bool halves) {
     if (nT == 0) return cudaSuccess;
-    const int threads = 128;
+    const int threads = kPreThreads;
     u64 blocks = (nT + threads - 1) / threads;
-    const u64 cap = (u64)sm_count(device) * 16;
+    const u64 cap = (u64)sm_count(device) * 32;
     if (blocks > cap) blocks = cap;
     k_tuple_precompute<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, T0, nT, out, halves);
     return cudaGetLastError();
@@ -1532,9 +1563,9 @@ cudaError_t launch_precompute_segs(cudaStream_t st, int device, const DevProblem
                                    int ng, const double* coef, const u64* seg, int nseg, u64 nT, TupleConst* out,
                                    bool halves) {
     if (nT == 0) return cudaSuccess;
-    const int threads = 128;
+    const int threads = kPreThreads;
     u64 blocks = (nT + threads - 1) / threads;
-    const u64 cap = (u64)sm_count(device) * 16;
+    const u64 cap = (u64)sm_count(device) * 32;
     if (blocks > cap) blocks = cap;
     k_tuple_precompute_segs<<<(unsigned)blocks, threads, 0, st>>>(P, groups, ng, coef, seg, nseg, nT, out, halves);
     return cudaGetLastError();
@@ -1730,9 +1761,9 @@ cudaError_t launch_eval(cudaStream_t st, int device, const DevProblem& P, const 
 
 cudaError_t launch_pilot_zero(cudaStream_t st, int device, const DevProblem& P, const EvalArgs& A) {
     if (A.n_units == 0) return cudaSuccess;
-    const int threads = 128;
+    const int threads = 64;                                 // k_pilot_zero's NT
     u64 blocks = (A.n_units + threads - 1) / threads;
-    const u64 cap = (u64)sm_count(device) * 8;
+    const u64 cap = (u64)sm_count(device) * 16;
     if (blocks > cap) blocks = cap;
     if (P.unit_factors)
         k_pilot_zero<true><<<(unsigned)blocks, threads, 0, st>>>(P, A);
