@@ -56,7 +56,7 @@ def alg_ops(phases: int, bound_rows: int, unit: bool) -> float:
 # same workload, committed under profiles/): DRAM traffic and pipe figures cannot
 # be measured live without a profiler, so they are READ from that file at run time
 # and labelled as a reference capture, never as this run's measurement.
-NCU_CAPTURE = {2: "profiles/r2/ncu_k_eval_q_r2ap_raw.csv"}
+NCU_CAPTURE = {2: "profiles/r2/ncu_k_eval_q_r2as_raw.csv"}
 _SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
           "ms": 1.0, "msecond": 1.0, "s": 1e3, "nsecond": 1e-6, "%": 1.0, "": 1.0}
 
