@@ -833,10 +833,11 @@ static mist_status_t sweep(mist_ctx_t* ctx, const Prepared& pp, const std::vecto
             if (*p == ',') ++p;
         }
     } else {
-        // measured (profiles/r1/ab_pl2_summary.txt): one level of 2 / 3 / 5 values up to Q < 40;
-        // for the Q = 50 space two levels {5, 11} (cfg5 windows -22% in sum vs one 7-value level)
+        // measured (profiles/r1/ab_pl2_summary.txt, r2/ab_pilot_levels_r2_summary.txt,
+        // r2/ab_pl4_summary.txt): one level of 2 / 3 / 4 / 5 values up to Q < 40 (Q = 8: 3,
+        // Q = 10: 4 since the round-2 filters); for the Q = 50 space two levels {5, 11}
         if (Q < 40) {
-            levels.push_back(Q < 8 ? 2 : Q < 16 ? 3 : 5);
+            levels.push_back(Q < 8 ? 2 : Q < 10 ? 3 : Q < 16 ? 4 : 5);
         } else {
             levels.push_back(5);
             levels.push_back(11);
